@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 AMS-Quant fused linear (BASELINE.json config 2 by default).
+
+A *step* is one pass over the Llama-3.1-8B layer linears (qkv 6144x4096, o 4096x4096,
+gate_up 28672x4096, down 4096x14336) at every batch M in {1, 4, 8, 16}: 16 fused
+restore+linear calls on FP5.33-e2m3 weights. ``value`` is packed-weight GB/s over the
+timed region (sum of reference-stream payload bytes / device time), inputs resident in
+HBM; ``e2e`` is the same metric through the C-ABI ``amsq_gemv_host`` with pinned host
+buffers (H2D x and D2H y inside the timed region). Weights rotate across two copies
+(>2x the 126 MB L2) so every call streams from HBM.
+
+``--impl reference`` times the reference's own CPU ``amsq::gemv`` (oracle/_ref, all host
+threads) on the same workload. Multi-GPU (torchrun): every rank runs the same workload on
+its own GPU (replicas, weak scaling; the TP all-gather path is ``--tp``).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPES_8B = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096),
+             "down": (4096, 14336)}
+SHAPES_70B = {"qkv": (10240, 8192), "o": (8192, 8192), "gate_up": (57344, 8192),
+              "down": (8192, 28672)}
+BATCHES = [1, 4, 8, 16]
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", 1375.8)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload data
+def make_payload(sid, rows, cols, seed):
+    """Random valid packed stream; FP5.33 padding codes zeroed."""
+    import paper_2510_16045_b200 as amsq
+    s = amsq.scheme_by_id(sid)
+    rng = np.random.default_rng(seed)
+    pc = amsq.round_up(cols, s.block)
+    wpr = pc // s.block * s.words_per_block
+    payload = rng.integers(0, 1 << 16, size=(rows, wpr), dtype=np.uint16)
+    if pc > cols:  # padding columns restore to 0: clear their code segments (keep shared = 0)
+        for c in range(cols, pc):
+            blk, j = divmod(c, s.block)
+            if sid == 7:
+                payload[:, blk] &= np.uint16(~(0x1F << (5 * j)) & 0x7FFF)
+            else:
+                raise NotImplementedError
+    scales = rng.uniform(0.002, 0.02, size=rows).astype(np.float16).view(np.uint16)
+    return amsq.QuantizedTensor(s, rows, cols, pc, scales, payload.reshape(-1))
+
+
+def algorithmic_bytes(payload_bytes, rows, cols, m):
+    return payload_bytes + 2 * rows + 2 * m * cols + 2 * m * rows
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.nn.functional as F
+
+    import paper_2510_16045_b200 as amsq
+    from paper_2510_16045_b200._lib import lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    sid = amsq.scheme_by_name(args.scheme).id
+    shapes = SHAPES_8B if args.model == "8b" else SHAPES_70B
+    batches = [int(b) for b in args.batches.split(",")]
+    copies = args.copies
+    # weights: `copies` independent sets so consecutive calls never hit L2
+    sets = []
+    for c in range(copies):
+        ws = {}
+        for i, (name, (n, k)) in enumerate(shapes.items()):
+            qt = make_payload(sid, n, k, seed=1000 * c + i + 17 * rank)
+            ws[name] = amsq.DeviceWeight(qt, device=local)
+        sets.append(ws)
+    payload_bytes = {name: sets[0][name].payload_bytes for name in shapes}
+    xs = {(name, m): torch.randn(m, k, device=dev).half() for name, (n, k) in shapes.items()
+          for m in batches}
+    ys = {(name, m): torch.empty(m, n, device=dev, dtype=torch.float16)
+          for name, (n, k) in shapes.items() for m in batches}
+    calls = [(name, m) for m in batches for name in shapes]
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step(i, ev=None):
+        ws = sets[i % copies]
+        for ci, (name, m) in enumerate(calls):
+            if ev is not None:
+                ev[ci][0].record(stream)
+            rc = lib().amsq_linear(ws[name].handle, xs[(name, m)].data_ptr(), m,
+                                   ys[(name, m)].data_ptr(), sp)
+            if rc:
+                raise RuntimeError(lib().amsq_last_error().decode())
+            if ev is not None:
+                ev[ci][1].record(stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+            for _ in calls] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = amsq.kernel_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i, evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = amsq.kernel_launch_count() - launches0
+    total_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    per_call = {c: [evs[i][ci][0].elapsed_time(evs[i][ci][1]) for i in range(args.steps)]
+                for ci, c in enumerate(calls)}
+    bytes_per_step = sum(payload_bytes[name] for name, m in calls)
+    value = world * bytes_per_step * args.steps / (total_ms * 1e-3) / 1e9
+
+    # --- cuBLAS FP16 baseline on the same shapes/rotation (F.linear -> cublasGemmEx)
+    dense = [{name: torch.randn(n, k, device=dev).half() for name, (n, k) in shapes.items()}
+             for _ in range(2)]
+    cub = {}
+    for name, m in calls:
+        ts = []
+        for i in range(args.warmup + args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            F.linear(xs[(name, m)], dense[i % 2][name])
+            b.record(stream)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        cub[(name, m)] = [a.elapsed_time(b) for a, b in ts[args.warmup:]]
+    del dense
+    torch.cuda.empty_cache()
+
+    peak, tpeak, peak_kind = _peaks()
+    detail = []
+    alg_total, t_total = 0.0, 0.0
+    for name, m in calls:
+        n, k = shapes[name]
+        us = statistics.median(per_call[(name, m)]) * 1e3
+        cub_us = statistics.median(cub[(name, m)]) * 1e3
+        alg = algorithmic_bytes(payload_bytes[name], n, k, m)
+        alg_total += alg * args.steps
+        t_total += sum(per_call[(name, m)]) * 1e-3
+        detail.append({"layer": name, "N": n, "K": k, "M": m, "us": round(us, 2),
+                       "packed_GBps": round(payload_bytes[name] / us / 1e3, 1),
+                       "alg_GBps": round(alg / us / 1e3, 1),
+                       "frac_of_peak": round(alg / us / 1e3 / peak, 3),
+                       "cublas_fp16_us": round(cub_us, 2),
+                       "speedup_vs_cublas": round(cub_us / us, 2)})
+    achieved = alg_total / t_total / 1e9
+
+    # --- end to end through the C-ABI with pinned host buffers
+    e2e = run_e2e(args, sets, shapes, calls, payload_bytes, dev, world)
+
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.scheme)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "AMS linear packed-weight HBM GB/s (Llama-3.1-8B qkv/o/gate_up/down, "
+                  "batch 1/4/8/16; per-call us and speedup vs FP16 cuBLAS in detail)",
+        "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic: random valid packed streams (FP5.33 padding zeroed), random fp16 x",
+        "config": {"workload": f"{args.scheme} linear, Llama-3.1-{args.model.upper()} layer "
+                               f"shapes x batch {args.batches}, 1 step = {len(calls)} calls",
+                   "scheme": args.scheme, "shapes": {k: list(v) for k, v in shapes.items()},
+                   "batches": batches,
+                   "l2": f"weights rotated over {copies} copies "
+                         f"({copies * sum(payload_bytes.values()) / 1e6:.0f} MB > 126 MB L2)",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "amsq_linear_kernel", "peak_kind": peak_kind,
+                     "bytes": "algorithmic = packed_payload_bytes + 2N + 2MK + 2MN per call"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "detail": detail,
+    }
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args, shapes, batches, sid, sample_only=True)
+    return line
+
+
+def run_e2e(args, sets, shapes, calls, payload_bytes, dev, world):
+    import torch
+
+    from paper_2510_16045_b200._lib import lib
+
+    stream = torch.cuda.current_stream()
+    hx = {(name, m): torch.randn(m, shapes[name][1]).half().pin_memory() for name, m in calls}
+    hy = {(name, m): torch.empty(m, shapes[name][0], dtype=torch.float16).pin_memory()
+          for name, m in calls}
+    h2d = sum(2 * m * shapes[name][1] for name, m in calls)
+    d2h = sum(2 * m * shapes[name][0] for name, m in calls)
+    steps = max(2, args.steps // 2)
+
+    def one(i):
+        ws = sets[i % len(sets)]
+        for name, m in calls:
+            rc = lib().amsq_gemv_host(ws[name].handle, hx[(name, m)].data_ptr(),
+                                      m * shapes[name][1], m, hy[(name, m)].data_ptr(),
+                                      stream.cuda_stream)
+            if rc:
+                raise RuntimeError(lib().amsq_last_error().decode())
+
+    for i in range(2):
+        one(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(steps):
+        one(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    val = world * sum(payload_bytes[n] for n, m in calls) * steps / (ms * 1e-3) / 1e9
+    return {"value": round(val, 1), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(ms / steps, 4),
+            "path": "amsq_gemv_host (pinned host x/y, H2D + kernel + D2H per call)"}
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def cpu_baseline(args, shapes, batches, sid, sample_only=True, steps=1, warmup=0):
+    """The reference's own amsq::gemv (oracle/_ref) on all host threads; falls back to the
+    plain-C oracle port (1 thread) when the reference was never compiled."""
+    from oracle import COracle, load_ref
+
+    ref = load_ref()
+    cores = os.cpu_count() or 1
+    kind = "reference" if ref is not None else "port"
+    calls = [(name, m) for m in batches for name in shapes]
+    if kind == "port":  # single-threaded C port: keep the sample bounded
+        calls = [("o", 1), ("qkv", 1)]
+    tensors = {}
+    for i, name in enumerate(shapes):
+        if any(c[0] == name for c in calls):
+            n, k = shapes[name]
+            tensors[name] = make_payload(sid, n, k, seed=i + 17)
+    total_bytes, total_s = 0, 0.0
+    if kind == "reference":
+        import ctypes as C
+        handles = {}
+        for name, qt in tensors.items():
+            handles[name] = ref.lib.ref_tensor_new(sid, qt.rows, qt.cols, qt.padded_cols,
+                                                   qt.scales, qt.payload, qt.payload.size)
+        threads = ref.lib.ref_resolve_threads(0)
+        for it in range(warmup + steps):
+            for name, m in calls:
+                n, k = shapes[name]
+                x = np.random.default_rng(m).standard_normal(m * k).astype(np.float16).view(np.uint16)
+                y = np.zeros(m * n, np.uint16)
+                t = time.perf_counter()
+                rc = ref.lib.ref_tensor_gemv(handles[name], x.ctypes.data, m, threads, y.ctypes.data)
+                dt = time.perf_counter() - t
+                if rc:
+                    raise RuntimeError("reference gemv failed")
+                if it >= warmup:
+                    total_bytes += tensors[name].payload.size * 2
+                    total_s += dt
+        for h in handles.values():
+            ref.lib.ref_tensor_free(h)
+        cores_used = threads
+        sample = (f"reference amsq::gemv (oracle/_ref, -O2 -ffp-contract=off), {len(calls)} calls "
+                  f"x {steps} pass(es): all layer shapes x batch {batches}, threads={threads}")
+    else:
+        orc = COracle()
+        for it in range(warmup + steps):
+            for name, m in calls:
+                qt = tensors[name]
+                x = np.random.default_rng(m).standard_normal(m * qt.cols).astype(np.float16).view(np.uint16)
+                t = time.perf_counter()
+                orc.gemv(sid, qt.rows, qt.cols, qt.padded_cols, qt.scales, qt.payload, x, m)
+                dt = time.perf_counter() - t
+                if it >= warmup:
+                    total_bytes += qt.payload.size * 2
+                    total_s += dt
+        cores_used = 1
+        sample = f"C oracle port, 1 thread, calls {calls}"
+    value = total_bytes / total_s / 1e9
+    return {"value": round(value, 4), "unit": "GB/s", "cores": int(cores_used),
+            "host_cores": cores, "kind": kind, "sample": sample,
+            "seconds": round(total_s, 2)}
+
+
+def run_reference_arm(args, world, rank):
+    import paper_2510_16045_b200 as amsq  # scheme table only (host)
+
+    if rank != 0:
+        return None
+    sid = amsq.scheme_by_name(args.scheme).id
+    shapes = SHAPES_8B if args.model == "8b" else SHAPES_70B
+    batches = [int(b) for b in args.batches.split(",")]
+    steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0
+    cb = cpu_baseline(args, shapes, batches, sid, steps=steps, warmup=warm)
+    n_calls = len(batches) * len(shapes)
+    return {
+        "impl": "reference",
+        "metric": "AMS linear packed-weight HBM GB/s (Llama-3.1-8B qkv/o/gate_up/down, "
+                  "batch 1/4/8/16; per-call us and speedup vs FP16 cuBLAS in detail)",
+        "value": cb["value"], "unit": "GB/s", "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": round(cb["seconds"] / steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic: random valid packed streams, random fp16 x",
+        "config": {"workload": f"{args.scheme} linear, Llama-3.1-{args.model.upper()} layer "
+                               f"shapes x batch {args.batches}, 1 step = {n_calls} calls",
+                   "scheme": args.scheme, "batches": batches},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scheme", default="fp5.33-e2m3")
+    ap.add_argument("--model", default="8b", choices=["8b", "70b"])
+    ap.add_argument("--batches", default="1,4,8,16")
+    ap.add_argument("--copies", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        line = run_reference_arm(args, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    line = run_ours(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

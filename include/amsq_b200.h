@@ -1,0 +1,180 @@
+/*
+ * amsq_b200.h -- C-ABI of the B200-native AMS-Quant weight-only linear.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/amsq): every entry point below names the
+ * reference interface it replaces. Plain pointers and sizes only; no C++ or
+ * torch types cross it. Device pointers are caller-owned and `stream` is a
+ * cudaStream_t (NULL = legacy default stream); all device entry points are
+ * stream-ordered and asynchronous unless stated otherwise.
+ *
+ * Errors: every function returns an amsq_status; amsq_last_error() gives the
+ * thread-local message of the last failure. The C++ wrapper (amsq_b200.hpp)
+ * maps AMSQ_EINVAL -> std::invalid_argument and everything else ->
+ * std::runtime_error, preserving the reference tests' exception types
+ * (SURVEY.md §8(b)).
+ */
+#ifndef AMSQ_B200_H_
+#define AMSQ_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AMSQ_OK = 0,
+  AMSQ_EINVAL = 1,   /* std::invalid_argument in the reference */
+  AMSQ_ECORRUPT = 2, /* std::runtime_error: data (shared-bit mismatch, non-finite, overflow, container) */
+  AMSQ_ECUDA = 3,    /* CUDA runtime / launch failure */
+  AMSQ_ENCCL = 4,    /* NCCL failure (tensor-parallel path) */
+  AMSQ_ENOMEM = 5,
+  AMSQ_ENODEV = 6    /* no CUDA device: the product never falls back to the CPU */
+} amsq_status;
+
+/* Scheme ids are the container/ABI enum of scheme.hpp:21-30. */
+enum {
+  AMSQ_FP4_E2M1 = 0,
+  AMSQ_FP5_E2M2 = 1,
+  AMSQ_FP6_E2M3 = 2,
+  AMSQ_FP6_E3M2 = 3,
+  AMSQ_FP4_25_E2M2 = 4,
+  AMSQ_FP4_33_E2M2 = 5,
+  AMSQ_FP4_5_E2M2 = 6,
+  AMSQ_FP5_33_E2M3 = 7
+};
+
+typedef struct {
+  int id;
+  int exp_bits, man_bits, bias; /* FloatFormat, format.hpp:31-72 */
+  int k;                        /* weights sharing one mantissa LSB */
+  size_t block;                 /* PackLayout::block, packing.hpp:51-63 */
+  size_t words_per_block;       /* PackLayout::words_per_block */
+  const char* name;             /* QuantScheme::name, scheme.hpp:59-74 */
+  int device_supported;         /* 1 if the sm_100a kernels implement this scheme */
+} amsq_scheme_info_t;
+
+const char* amsq_last_error(void);
+const char* amsq_version(void);
+
+/* ---- scheme / layout metadata (scheme.hpp:76-89, packing.hpp:143-157, quantize.hpp:64-69) */
+int amsq_scheme_info(int scheme_id, amsq_scheme_info_t* out);
+int amsq_scheme_by_name(const char* name, int* scheme_id);
+size_t amsq_packed_payload_bytes(int scheme_id, size_t rows, size_t cols);
+
+/* ---- binary16 (half.hpp:16-71) */
+uint16_t amsq_float_to_half(float f);
+float amsq_half_to_float(uint16_t h);
+/* to_fp16_bits / restore_table (format.hpp:190-198): table[code], n >= 2^(1+e+m) */
+int amsq_restore_table(int scheme_id, uint16_t* table, size_t n);
+
+/* ---- host codec of the reference stream (packing.hpp:216-266) */
+int amsq_pack_row(int scheme_id, const uint8_t* codes, size_t n_codes, uint16_t* words,
+                  size_t n_words);
+int amsq_unpack_row(int scheme_id, const uint16_t* words, size_t n_words, uint8_t* codes,
+                    size_t n_codes);
+
+/* ---- host quantizer, kept on the host by design (quantize.hpp:188-216 quantize_tensor:
+ * RTN + Adaptive Searching + pack). `w` is row-major [rows][cols] fp32. Pass
+ * scales == payload == NULL to query *padded_cols and *payload_words. threads <= 0
+ * means all hardware threads (parallel.hpp:15-19). */
+int amsq_quantize_tensor(int scheme_id, size_t rows, size_t cols, const float* w, int threads,
+                         size_t* padded_cols, size_t* payload_words, uint16_t* scales,
+                         uint16_t* payload);
+
+/* ---- AMSQ container v1 (container.hpp:63-127), host buffers. */
+int amsq_container_size(int scheme_id, size_t rows, size_t cols, size_t* bytes);
+int amsq_container_write(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
+                         const uint16_t* scales, const uint16_t* payload, size_t payload_words,
+                         uint8_t* out, size_t out_bytes);
+/* Validating reader: parses the header into the outputs; copies scales/payload when the
+ * pointers are non-NULL (sizes checked). */
+int amsq_container_read(const uint8_t* in, size_t in_bytes, int* scheme_id, size_t* rows,
+                        size_t* cols, size_t* padded_cols, uint16_t* scales, size_t n_scales,
+                        uint16_t* payload, size_t payload_words);
+
+/* ---- the device tile layout on the host: exposed so the layout and its
+ * exact inverse can be checked without a GPU. tiles must hold amsq_device_layout_bytes(). */
+size_t amsq_device_layout_bytes(int scheme_id, size_t rows, size_t cols);
+int amsq_repack(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
+                const uint16_t* payload, size_t payload_words, uint8_t* tiles, size_t tile_bytes);
+int amsq_unrepack(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
+                  const uint8_t* tiles, size_t tile_bytes, uint16_t* payload,
+                  size_t payload_words);
+
+/* ---- device weights: the QuantizedTensor (quantize.hpp:45-61) uploaded into the
+ * sm_100a tile layout. The repack is a pure bit permutation of the
+ * reference stream: amsq_weight_download() returns the identical words. */
+typedef struct amsq_weight_s* amsq_weight_t;
+
+int amsq_weight_upload(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
+                       const uint16_t* scales, const uint16_t* payload, size_t payload_words,
+                       int device, void* stream, amsq_weight_t* out);
+/* N-shard [row0, row0+nrows) of a full tensor (column-parallel TP). */
+int amsq_weight_upload_rows(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
+                            const uint16_t* scales, const uint16_t* payload,
+                            size_t payload_words, size_t row0, size_t nrows, int device,
+                            void* stream, amsq_weight_t* out);
+/* Container bytes -> device in one step (container.hpp:79-115 read_amsq + upload). */
+int amsq_weight_upload_container(const uint8_t* in, size_t in_bytes, size_t row0, size_t nrows,
+                                 int device, void* stream, amsq_weight_t* out);
+int amsq_weight_download(amsq_weight_t h, uint16_t* scales, size_t n_scales, uint16_t* payload,
+                         size_t payload_words);
+int amsq_weight_free(amsq_weight_t h);
+
+typedef struct {
+  int scheme_id;
+  size_t rows, cols, padded_cols;
+  size_t payload_bytes;        /* reference stream bytes, packed_payload_bytes() */
+  size_t device_bytes;         /* bytes of the device tile layout (>= payload_bytes) */
+  size_t row_tiles, k_tiles;   /* 16-row x (64|48)-col tiles */
+  int device;
+} amsq_weight_info_t;
+int amsq_weight_info(amsq_weight_t h, amsq_weight_info_t* out);
+
+/* ---- the hot path (kernels.hpp), device buffers, stream-ordered ----------------- */
+
+/* restore_block over the whole tensor (kernels.hpp:55-63): binary16 grid bits,
+ * [rows][padded_cols]. Bit-exact bar #1. */
+int amsq_restore_grid_f16(amsq_weight_t h, uint16_t* d_out, void* stream);
+/* restore_matrix (kernels.hpp:100-124): fp32 w*s, [rows][cols]. Bit-exact. */
+int amsq_restore_f32(amsq_weight_t h, float* d_out, void* stream);
+/* restore_matrix_half (kernels.hpp:127-133): fp16(w*s), [rows][cols]. Bit-exact. */
+int amsq_restore_f16(amsq_weight_t h, uint16_t* d_out, void* stream);
+
+/* gemv (kernels.hpp:151-187): y[b][r] = fp16(sum_i w_i s_r x_b,i), fp32 accumulation.
+ * d_x is [batch][cols] fp16 (logical cols), d_y is [batch][rows] fp16.
+ * batch >= 1 (check_gemv_shapes, kernels.hpp:137-143 -> AMSQ_EINVAL). */
+int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream);
+
+/* Same with an explicit output row stride (elements) for writing into a wider buffer. */
+int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y,
+                   size_t ldy, void* stream);
+
+/* The reference call shape end to end: host x in, host y out (H2D, kernel, D2H on
+ * `stream`, synchronous on return). x_len must equal batch*cols. */
+int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batch, uint16_t* y,
+                   void* stream);
+
+/* ---- column-parallel tensor parallelism ----------------------
+ * `shard` holds rows [rank*N/P, (rank+1)*N/P). Computes the local [batch][N/P] output,
+ * all-gathers it with ncclAllGather over `nccl_comm` (an ncclComm_t), and writes the
+ * reference-layout [batch][N] result into d_y. d_scratch must hold
+ * 2*batch*(N/P)*(P+1) bytes. */
+int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint16_t* d_y,
+                   void* d_scratch, size_t scratch_bytes, void* nccl_comm, int nranks,
+                   void* stream);
+/* [P][batch][n] -> [batch][P*n] permutation used after the gather (exposed for tests). */
+int amsq_tp_unshard(const uint16_t* d_gathered, size_t nranks, size_t batch, size_t n_local,
+                    uint16_t* d_y, void* stream);
+
+/* Number of this library's kernels launched so far in this process (bench accounting). */
+uint64_t amsq_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMSQ_B200_H_ */

@@ -1,0 +1,513 @@
+// capi.cu -- implementation of the C-ABI declared in include/amsq_b200.h.
+//
+// Exceptions never cross the boundary: InvalidArgument -> AMSQ_EINVAL, Corrupt ->
+// AMSQ_ECORRUPT, CUDA/NCCL failures -> AMSQ_ECUDA/AMSQ_ENCCL, with a thread-local
+// message. Device entry points never fall back to the CPU: without a device they
+// fail with AMSQ_ENODEV.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "amsq_b200.h"
+#include "device_layout.hpp"
+#include "host_core.hpp"
+#include "kernels.h"
+
+struct amsq_weight_s {
+  amsqb::DeviceLayout L;
+  int device = 0;
+  uint8_t* d_w = nullptr;
+  unsigned short* d_scales = nullptr;
+  float* d_partials = nullptr;
+  int* d_counters = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CudaError : std::runtime_error {
+  cudaError_t code;
+  CudaError(cudaError_t c, const char* what)
+      : std::runtime_error(std::string(what) + ": " + cudaGetErrorString(c)), code(c) {}
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(e, what);
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return AMSQ_OK;
+  } catch (const amsqb::InvalidArgument& e) {
+    g_error = e.what();
+    return AMSQ_EINVAL;
+  } catch (const amsqb::Corrupt& e) {
+    g_error = e.what();
+    return AMSQ_ECORRUPT;
+  } catch (const NoDevice& e) {
+    g_error = e.what();
+    return AMSQ_ENODEV;
+  } catch (const NcclError& e) {
+    g_error = e.what();
+    return AMSQ_ENCCL;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return e.code == cudaErrorMemoryAllocation ? AMSQ_ENOMEM : AMSQ_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return AMSQ_ENOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return AMSQ_ECORRUPT;
+  }
+}
+
+void require_device(int device) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    throw NoDevice(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                   "): the AMS-Quant kernels run on sm_100a only, there is no CPU fallback");
+  }
+  if (device < 0 || device >= n) throw amsqb::InvalidArgument("device index out of range");
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) {
+    throw NoDevice("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                   "; this library is built for sm_100a (B200) only");
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_handle(amsq_weight_t h) {
+  if (!h || !h->d_w) throw amsqb::InvalidArgument("null weight handle");
+}
+
+amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
+                          const uint16_t* scales, const uint16_t* payload, size_t words,
+                          size_t row0, size_t nrows, int device, void* stream) {
+  const amsqb::Scheme& s = amsqb::scheme(scheme_id);
+  if (!scales || !payload) throw amsqb::InvalidArgument("upload: null host buffer");
+  if (rows == 0 || cols == 0) throw amsqb::InvalidArgument("upload: empty tensor");
+  if (pc != amsqb::padded_cols(s, cols)) throw amsqb::InvalidArgument("upload: padded_cols mismatch");
+  const size_t wpr = amsqb::words_per_row(s, pc);
+  if (words != rows * wpr) throw amsqb::InvalidArgument("upload: payload size mismatch");
+  if (nrows == 0 || row0 + nrows > rows) throw amsqb::InvalidArgument("upload: row range out of bounds");
+  require_device(device);
+  DeviceGuard dg(device);
+  auto h = std::make_unique<amsq_weight_s>();
+  h->device = device;
+  h->L = amsqb::make_device_layout(scheme_id, nrows, cols, pc);
+  std::vector<uint8_t> tiles(h->L.bytes());
+  amsqb::repack_to_device(h->L, payload + row0 * wpr, tiles.data(), 0);
+  std::vector<unsigned short> sc(h->L.row_tiles * 16, 0);
+  std::memcpy(sc.data(), scales + row0, nrows * sizeof(uint16_t));
+  const size_t grid = static_cast<size_t>(amsqb::linear_grid(
+      static_cast<long long>(h->L.row_blocks() * h->L.k_tiles)));
+  const size_t partial_floats = (grid + h->L.row_blocks()) * 16 * 256;
+  cudaStream_t st = as_stream(stream);
+  ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");
+  ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
+  ck(cudaMalloc(&h->d_partials, partial_floats * sizeof(float)), "cudaMalloc(partials)");
+  ck(cudaMalloc(&h->d_counters, h->L.row_blocks() * sizeof(int)), "cudaMalloc(counters)");
+  ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
+  ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
+  ck(cudaMemsetAsync(h->d_counters, 0, h->L.row_blocks() * sizeof(int), st), "memset counters");
+  ck(cudaStreamSynchronize(st), "upload sync");  // host staging buffers die here
+  return h.release();
+}
+
+void free_impl(amsq_weight_t h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  cudaFree(h->d_w);
+  cudaFree(h->d_scales);
+  cudaFree(h->d_partials);
+  cudaFree(h->d_counters);
+  delete h;
+}
+
+void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,
+                 cudaStream_t st) {
+  check_handle(h);
+  if (batch == 0) throw amsqb::InvalidArgument("gemv: activation shape mismatch");
+  if (!d_x || !d_y) throw amsqb::InvalidArgument("linear: null device buffer");
+  if (ldy < h->L.rows) throw amsqb::InvalidArgument("linear: ldy < rows");
+  DeviceGuard dg(h->device);
+  amsqb::LinearParams p{};
+  p.scheme_id = h->L.scheme_id;
+  p.w = h->d_w;
+  p.scales = h->d_scales;
+  p.partials = h->d_partials;
+  p.counters = h->d_counters;
+  p.rows = static_cast<long long>(h->L.rows);
+  p.cols = static_cast<long long>(h->L.cols);
+  p.ldx = p.cols;
+  p.ldy = static_cast<long long>(ldy);
+  p.row_blocks = static_cast<int>(h->L.row_blocks());
+  p.k_tiles = static_cast<int>(h->L.k_tiles);
+  const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
+  for (size_t b0 = 0; b0 < batch; b0 += step) {
+    const size_t mb = batch - b0 < step ? batch - b0 : step;
+    p.x = reinterpret_cast<const unsigned short*>(d_x) + b0 * h->L.cols;
+    p.y = reinterpret_cast<unsigned short*>(d_y) + b0 * ldy;
+    p.M = static_cast<int>(mb);
+    ck(amsqb::launch_linear(p, st), "amsq_linear_kernel launch");
+  }
+}
+
+void restore_impl(amsq_weight_t h, uint16_t* grid, float* f32, uint16_t* f16, cudaStream_t st) {
+  check_handle(h);
+  DeviceGuard dg(h->device);
+  amsqb::RestoreParams p{};
+  p.scheme_id = h->L.scheme_id;
+  p.w = h->d_w;
+  p.scales = h->d_scales;
+  p.rows = static_cast<long long>(h->L.rows);
+  p.cols = static_cast<long long>(h->L.cols);
+  p.padded_cols = static_cast<long long>(h->L.padded_cols);
+  p.row_tiles = static_cast<int>(h->L.row_tiles);
+  p.k_tiles = static_cast<int>(h->L.k_tiles);
+  p.grid_out = reinterpret_cast<unsigned short*>(grid);
+  p.f32_out = f32;
+  p.f16_out = reinterpret_cast<unsigned short*>(f16);
+  ck(amsqb::launch_restore(p, st), "amsq_restore_kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* amsq_last_error(void) { return g_error.c_str(); }
+const char* amsq_version(void) { return "amsq-b200 0.1 (sm_100a)"; }
+
+int amsq_scheme_info(int id, amsq_scheme_info_t* out) {
+  return guarded([&] {
+    if (!out) throw amsqb::InvalidArgument("null output");
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    out->id = s.id;
+    out->exp_bits = s.exp_bits;
+    out->man_bits = s.man_bits;
+    out->bias = s.bias;
+    out->k = s.k;
+    out->block = static_cast<size_t>(s.block);
+    out->words_per_block = static_cast<size_t>(s.words_per_block);
+    out->name = s.name;
+    out->device_supported = amsqb::device_scheme_supported(id) ? 1 : 0;
+  });
+}
+
+int amsq_scheme_by_name(const char* name, int* id) {
+  return guarded([&] {
+    if (!name || !id) throw amsqb::InvalidArgument("null argument");
+    *id = amsqb::scheme_id_by_name(name);
+  });
+}
+
+size_t amsq_packed_payload_bytes(int id, size_t rows, size_t cols) {
+  if (id < 0 || id >= amsqb::kNumSchemes) return 0;
+  return amsqb::packed_payload_bytes(amsqb::scheme(id), rows, cols);
+}
+
+uint16_t amsq_float_to_half(float f) { return amsqb::f32_to_f16(f); }
+float amsq_half_to_float(uint16_t h) { return amsqb::f16_to_f32(h); }
+
+int amsq_restore_table(int id, uint16_t* table, size_t n) {
+  return guarded([&] {
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    if (!table || n < s.code_count()) throw amsqb::InvalidArgument("restore_table: buffer too small");
+    for (unsigned c = 0; c < s.code_count(); ++c) table[c] = amsqb::code_to_f16(s, c);
+  });
+}
+
+int amsq_pack_row(int id, const uint8_t* codes, size_t n, uint16_t* words, size_t nw) {
+  return guarded([&] {
+    amsqb::pack_row(amsqb::scheme(id), std::span<const uint8_t>(codes, n),
+                    std::span<uint16_t>(words, nw));
+  });
+}
+
+int amsq_unpack_row(int id, const uint16_t* words, size_t nw, uint8_t* codes, size_t n) {
+  return guarded([&] {
+    amsqb::unpack_row(amsqb::scheme(id), std::span<const uint16_t>(words, nw),
+                      std::span<uint8_t>(codes, n));
+  });
+}
+
+int amsq_quantize_tensor(int id, size_t rows, size_t cols, const float* w, int threads,
+                         size_t* padded, size_t* words, uint16_t* scales, uint16_t* payload) {
+  return guarded([&] {
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    if (rows == 0 || cols == 0) throw amsqb::InvalidArgument("quantize_tensor: empty matrix");
+    const size_t pc = amsqb::padded_cols(s, cols);
+    const size_t nw = rows * amsqb::words_per_row(s, pc);
+    if (padded) *padded = pc;
+    if (words) *words = nw;
+    if (!scales && !payload) return;
+    if (!scales || !payload || !w) throw amsqb::InvalidArgument("quantize_tensor: null buffer");
+    auto q = amsqb::quantize_tensor(s, rows, cols, w, threads);
+    std::memcpy(scales, q.scales.data(), rows * sizeof(uint16_t));
+    std::memcpy(payload, q.payload.data(), nw * sizeof(uint16_t));
+  });
+}
+
+int amsq_container_size(int id, size_t rows, size_t cols, size_t* bytes) {
+  return guarded([&] { *bytes = amsqb::container_bytes(amsqb::scheme(id), rows, cols); });
+}
+
+int amsq_container_write(int id, size_t rows, size_t cols, size_t pc, const uint16_t* scales,
+                         const uint16_t* payload, size_t words, uint8_t* out, size_t out_bytes) {
+  return guarded([&] {
+    amsqb::container_write(amsqb::scheme(id), rows, cols, pc, scales, payload, words, out, out_bytes);
+  });
+}
+
+int amsq_container_read(const uint8_t* in, size_t n, int* id, size_t* rows, size_t* cols,
+                        size_t* pc, uint16_t* scales, size_t n_scales, uint16_t* payload,
+                        size_t words) {
+  return guarded([&] {
+    if (!in) throw amsqb::InvalidArgument("null container");
+    const auto v = amsqb::container_parse(in, n);
+    if (id) *id = v.scheme_id;
+    if (rows) *rows = v.rows;
+    if (cols) *cols = v.cols;
+    if (pc) *pc = v.padded_cols;
+    if (scales) {
+      if (n_scales != v.rows) throw amsqb::InvalidArgument("container_read: scales size mismatch");
+      for (size_t i = 0; i < v.rows; ++i) scales[i] = static_cast<uint16_t>(v.scales[2 * i] | v.scales[2 * i + 1] << 8);
+    }
+    if (payload) {
+      if (words != v.payload_words) throw amsqb::InvalidArgument("container_read: payload size mismatch");
+      for (size_t i = 0; i < words; ++i) payload[i] = static_cast<uint16_t>(v.payload[2 * i] | v.payload[2 * i + 1] << 8);
+    }
+  });
+}
+
+size_t amsq_device_layout_bytes(int id, size_t rows, size_t cols) {
+  try {
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    return amsqb::make_device_layout(id, rows, cols, amsqb::padded_cols(s, cols)).bytes();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 0;
+  }
+}
+
+int amsq_repack(int id, size_t rows, size_t cols, size_t pc, const uint16_t* payload,
+                size_t words, uint8_t* tiles, size_t tile_bytes) {
+  return guarded([&] {
+    const auto L = amsqb::make_device_layout(id, rows, cols, pc);
+    if (words != rows * L.wpr) throw amsqb::InvalidArgument("repack: payload size mismatch");
+    if (tile_bytes != L.bytes()) throw amsqb::InvalidArgument("repack: tile buffer size mismatch");
+    amsqb::repack_to_device(L, payload, tiles, 0);
+  });
+}
+
+int amsq_unrepack(int id, size_t rows, size_t cols, size_t pc, const uint8_t* tiles,
+                  size_t tile_bytes, uint16_t* payload, size_t words) {
+  return guarded([&] {
+    const auto L = amsqb::make_device_layout(id, rows, cols, pc);
+    if (words != rows * L.wpr) throw amsqb::InvalidArgument("unrepack: payload size mismatch");
+    if (tile_bytes != L.bytes()) throw amsqb::InvalidArgument("unrepack: tile buffer size mismatch");
+    amsqb::repack_from_device(L, tiles, payload, 0);
+  });
+}
+
+int amsq_weight_upload(int id, size_t rows, size_t cols, size_t pc, const uint16_t* scales,
+                       const uint16_t* payload, size_t words, int device, void* stream,
+                       amsq_weight_t* out) {
+  return guarded([&] {
+    if (!out) throw amsqb::InvalidArgument("null output handle");
+    *out = upload_impl(id, rows, cols, pc, scales, payload, words, 0, rows, device, stream);
+  });
+}
+
+int amsq_weight_upload_rows(int id, size_t rows, size_t cols, size_t pc, const uint16_t* scales,
+                            const uint16_t* payload, size_t words, size_t row0, size_t nrows,
+                            int device, void* stream, amsq_weight_t* out) {
+  return guarded([&] {
+    if (!out) throw amsqb::InvalidArgument("null output handle");
+    *out = upload_impl(id, rows, cols, pc, scales, payload, words, row0, nrows, device, stream);
+  });
+}
+
+int amsq_weight_upload_container(const uint8_t* in, size_t n, size_t row0, size_t nrows,
+                                 int device, void* stream, amsq_weight_t* out) {
+  return guarded([&] {
+    if (!out || !in) throw amsqb::InvalidArgument("null argument");
+    const auto v = amsqb::container_parse(in, n);
+    std::vector<uint16_t> scales(v.rows), payload(v.payload_words);
+    for (size_t i = 0; i < v.rows; ++i) scales[i] = static_cast<uint16_t>(v.scales[2 * i] | v.scales[2 * i + 1] << 8);
+    for (size_t i = 0; i < v.payload_words; ++i) payload[i] = static_cast<uint16_t>(v.payload[2 * i] | v.payload[2 * i + 1] << 8);
+    if (nrows == 0) nrows = v.rows - row0;
+    *out = upload_impl(v.scheme_id, v.rows, v.cols, v.padded_cols, scales.data(), payload.data(),
+                       payload.size(), row0, nrows, device, stream);
+  });
+}
+
+int amsq_weight_download(amsq_weight_t h, uint16_t* scales, size_t n_scales, uint16_t* payload,
+                         size_t words) {
+  return guarded([&] {
+    check_handle(h);
+    DeviceGuard dg(h->device);
+    const auto& L = h->L;
+    if (scales) {
+      if (n_scales != L.rows) throw amsqb::InvalidArgument("download: scales size mismatch");
+      ck(cudaMemcpy(scales, h->d_scales, L.rows * 2, cudaMemcpyDeviceToHost), "D2H scales");
+    }
+    if (payload) {
+      if (words != L.rows * L.wpr) throw amsqb::InvalidArgument("download: payload size mismatch");
+      std::vector<uint8_t> tiles(L.bytes());
+      ck(cudaMemcpy(tiles.data(), h->d_w, tiles.size(), cudaMemcpyDeviceToHost), "D2H weights");
+      amsqb::repack_from_device(L, tiles.data(), payload, 0);
+    }
+  });
+}
+
+int amsq_weight_free(amsq_weight_t h) {
+  return guarded([&] { free_impl(h); });
+}
+
+int amsq_weight_info(amsq_weight_t h, amsq_weight_info_t* out) {
+  return guarded([&] {
+    check_handle(h);
+    if (!out) throw amsqb::InvalidArgument("null output");
+    const auto& L = h->L;
+    out->scheme_id = L.scheme_id;
+    out->rows = L.rows;
+    out->cols = L.cols;
+    out->padded_cols = L.padded_cols;
+    out->payload_bytes = L.rows * L.wpr * 2;
+    out->device_bytes = L.bytes();
+    out->row_tiles = L.row_tiles;
+    out->k_tiles = L.k_tiles;
+    out->device = h->device;
+  });
+}
+
+int amsq_restore_grid_f16(amsq_weight_t h, uint16_t* d_out, void* stream) {
+  return guarded([&] {
+    if (!d_out) throw amsqb::InvalidArgument("null output");
+    restore_impl(h, d_out, nullptr, nullptr, as_stream(stream));
+  });
+}
+
+int amsq_restore_f32(amsq_weight_t h, float* d_out, void* stream) {
+  return guarded([&] {
+    if (!d_out) throw amsqb::InvalidArgument("null output");
+    restore_impl(h, nullptr, d_out, nullptr, as_stream(stream));
+  });
+}
+
+int amsq_restore_f16(amsq_weight_t h, uint16_t* d_out, void* stream) {
+  return guarded([&] {
+    if (!d_out) throw amsqb::InvalidArgument("null output");
+    restore_impl(h, nullptr, nullptr, d_out, as_stream(stream));
+  });
+}
+
+int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    linear_impl(h, d_x, batch, d_y, h->L.rows, as_stream(stream));
+  });
+}
+
+int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,
+                   void* stream) {
+  return guarded([&] { linear_impl(h, d_x, batch, d_y, ldy, as_stream(stream)); });
+}
+
+int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batch, uint16_t* y,
+                   void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    if (batch == 0 || x_len != batch * h->L.cols) {
+      throw amsqb::InvalidArgument("gemv: activation shape mismatch");  // kernels.hpp:137-143
+    }
+    if (!x || !y) throw amsqb::InvalidArgument("gemv: null host buffer");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = as_stream(stream);
+    void* dx = nullptr;
+    void* dy = nullptr;
+    ck(cudaMallocAsync(&dx, x_len * 2, st), "cudaMallocAsync(x)");
+    ck(cudaMallocAsync(&dy, batch * h->L.rows * 2, st), "cudaMallocAsync(y)");
+    ck(cudaMemcpyAsync(dx, x, x_len * 2, cudaMemcpyHostToDevice, st), "H2D x");
+    linear_impl(h, static_cast<const uint16_t*>(dx), batch, static_cast<uint16_t*>(dy), h->L.rows, st);
+    ck(cudaMemcpyAsync(y, dy, batch * h->L.rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
+    ck(cudaFreeAsync(dx, st), "cudaFreeAsync");
+    ck(cudaFreeAsync(dy, st), "cudaFreeAsync");
+    ck(cudaStreamSynchronize(st), "gemv sync");
+  });
+}
+
+int amsq_tp_unshard(const uint16_t* d_in, size_t P, size_t batch, size_t n, uint16_t* d_y,
+                    void* stream) {
+  return guarded([&] {
+    if (!d_in || !d_y) throw amsqb::InvalidArgument("null buffer");
+    ck(amsqb::launch_unshard(reinterpret_cast<const unsigned short*>(d_in), static_cast<int>(P),
+                             static_cast<int>(batch), static_cast<int>(n),
+                             reinterpret_cast<unsigned short*>(d_y), as_stream(stream)),
+       "unshard launch");
+  });
+}
+
+int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint16_t* d_y,
+                   void* d_scratch, size_t scratch_bytes, void* nccl_comm, int nranks,
+                   void* stream) {
+  return guarded([&] {
+    check_handle(shard);
+    if (nranks < 1) throw amsqb::InvalidArgument("linear_tp: nranks < 1");
+    if (!nccl_comm && nranks > 1) throw amsqb::InvalidArgument("linear_tp: null communicator");
+    const size_t n = shard->L.rows;
+    const size_t need = 2 * batch * n * (static_cast<size_t>(nranks) + 1);
+    if (!d_scratch || scratch_bytes < need) throw amsqb::InvalidArgument("linear_tp: scratch too small");
+    cudaStream_t st = as_stream(stream);
+    if (nranks == 1) {
+      linear_impl(shard, d_x, batch, d_y, n, st);
+      return;
+    }
+    uint16_t* local = static_cast<uint16_t*>(d_scratch);
+    uint16_t* gathered = local + batch * n;
+    linear_impl(shard, d_x, batch, local, n, st);
+    DeviceGuard dg(shard->device);
+    const ncclResult_t r = ncclAllGather(local, gathered, batch * n, ncclFloat16,
+                                         static_cast<ncclComm_t>(nccl_comm), st);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    ck(amsqb::launch_unshard(gathered, nranks, static_cast<int>(batch), static_cast<int>(n),
+                             reinterpret_cast<unsigned short*>(d_y), st),
+       "unshard launch");
+  });
+}
+
+uint64_t amsq_kernel_launch_count(void) { return amsqb::kernel_launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// device_layout.hpp -- the sm_100a tile layout of the packed weights.
+//
+// The reference stream (packing.hpp:6-25; rows of `words_per_row` u16) is permuted,
+// bit for bit, into 16-row x TK-column tiles whose bytes are exactly what one warp's
+// mma.sync A-fragments need: lane (g = lane/4, t = lane%4) owns rows g and g+8 and
+// four reference groups of each, as four 32-bit registers R0..R3 (16 B, one
+// LDS.128). Each register holds two groups (a, b) of one row: output fp16x2 i of R is
+// (a_i, b_i), so the shared LSB of a lands in bit 8/7 of the low half and b's in the
+// high half. The bit positions inside R are chosen so that each fp16x2 is produced
+// by at most {mask, IMAD, LOP3} (see decode_* in kernels_common.cuh).
+//
+//  FP4.25-e2m2 (scheme 4): TK = 64 (one reference block per row), 544 B per tile:
+//    [lane*16, +16) R0..R3 (row g groups 4t,4t+1 | row g 4t+2,4t+3 | row g+8 ... )
+//    [512 + lane]   shared byte: bit r = group a of R_r, bit r+4 = group b of R_r
+//    R bits for member i (nibble = code bits 4..1 = s,E1,E0,M1; mag3 = E1,E0,M1):
+//      i=0: mag3<<9,  sign@15 | high: mag3<<25, sign@31
+//      i=1: mag3<<6,  sign@12 | high: mag3<<22, sign@28
+//      i=2: mag3<<3,  sign@13 | high: mag3<<19, sign@29
+//      i=3: mag3<<0,  sign@14 | high: mag3<<16, sign@30
+//  FP5.33-e2m3 (scheme 7): TK = 48 (16 reference words per row), 512 B per tile:
+//    [lane*16, +16) R0..R3, same row/group assignment, 2 reference words per R
+//    R bits for member i (seg = code bits 5..1 = s,E1,E0,M2,M1; mag4 = E1,E0,M2,M1):
+//      i=0: mag4<<8, sign@15            | high: mag4<<24, sign@31
+//      i=1: mag4<<0, sign@7             | high: mag4<<16, sign@23
+//      i=2: (mag4>>1)<<4, M1@13, sign@14 | high: (mag4>>1)<<20, M1@29, sign@30
+//      shared: a@12, b@28
+//
+// Tiles are stored [row_tile][k_tile] so one row tile's K range is one contiguous
+// run (a single cp.async.bulk per stage). Row tiles are padded to a multiple of 16
+// (256-row blocks), K to a multiple of TK; padding is zero and restores to +0.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace amsqb {
+
+struct DeviceLayout {
+  int scheme_id = -1;
+  size_t rows = 0, cols = 0, padded_cols = 0;
+  size_t wpr = 0;        // reference words per row
+  size_t tk = 0;         // columns per k-tile
+  size_t tile_bytes = 0;
+  size_t row_tiles = 0;  // padded to a multiple of kRowTilesPerBlock
+  size_t k_tiles = 0;
+  size_t row_blocks() const { return row_tiles / 16; }
+  size_t bytes() const { return row_tiles * k_tiles * tile_bytes; }
+};
+
+constexpr size_t kRowsPerTile = 16;
+constexpr size_t kRowTilesPerBlock = 16;  // 256-row blocks (8 warps x 2 row tiles)
+
+bool device_scheme_supported(int scheme_id);
+DeviceLayout make_device_layout(int scheme_id, size_t rows, size_t cols, size_t padded_cols);
+
+// payload: reference rows [rows][wpr] (row-major). out: layout.bytes() bytes.
+void repack_to_device(const DeviceLayout& L, const uint16_t* payload, uint8_t* out, int threads);
+// Exact inverse: writes [rows][wpr].
+void repack_from_device(const DeviceLayout& L, const uint8_t* in, uint16_t* payload, int threads);
+
+}  // namespace amsqb

@@ -1,0 +1,172 @@
+"""GPU parity tests of the sm_100a kernels against the oracle (run on the B200).
+
+Bars: restore is bit-exact (grid bits vs restore_block, fp32 w*s vs
+restore_matrix, fp16 vs restore_matrix_half); the fused linear is within
+norm-wise 1e-3 and per-element 1e-3*sum|w s x| + 1 ulp of the reference gemv.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_16045_b200 as amsq
+from helpers import check_linear, gaussian_x, quantized_gaussian, random_payload
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = [4, 7]
+SHAPES = [(1, 64), (33, 200), (40, 100), (16, 48), (300, 1000), (257, 4096), (512, 4098)]
+
+
+def _grid(dw):
+    return dw.restore_grid().cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("shape", SHAPES)
+def test_restore_grid_bit_exact(cuda, orc, sid, shape):
+    rows, cols = shape
+    for qt in (quantized_gaussian(sid, rows, cols, seed=rows + cols),
+               random_payload(sid, rows, cols, seed=rows * 7 + cols)):
+        dw = amsq.DeviceWeight(qt)
+        got = _grid(dw)
+        want = orc.restore_grid(sid, rows, qt.padded_cols, qt.payload)
+        assert np.array_equal(got, want), f"{(got != want).sum()} mismatching grid elements"
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_restore_every_code_exhaustively(cuda, orc, sid):
+    """kernels_test.cc:69-87 on the device: a block repeating one code, for every code."""
+    s = amsq.scheme_by_id(sid)
+    codes = np.repeat(np.arange(s.code_count, dtype=np.uint8), s.block)
+    # consistent shared bits per group are guaranteed by repeating one code per block
+    words = np.concatenate([amsq.pack_row(codes[i * s.block:(i + 1) * s.block], s)
+                            for i in range(s.code_count)])
+    rows = 16
+    cols = s.code_count * s.block
+    payload = np.tile(words, rows)
+    qt = amsq.QuantizedTensor(s, rows, cols, cols, np.full(rows, 0x3C00, np.uint16), payload)
+    got = _grid(amsq.DeviceWeight(qt))
+    table = amsq.restore_table(s)
+    want = np.tile(table[codes], (rows, 1))
+    assert np.array_equal(got, want)
+    assert np.array_equal(table, orc.restore_table(sid))
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("shape", [(33, 200), (300, 1000), (64, 4096)])
+def test_restore_matrix_f32_f16_bit_exact(cuda, orc, ref, sid, shape):
+    rows, cols = shape
+    qt = quantized_gaussian(sid, rows, cols, seed=11)
+    dw = amsq.DeviceWeight(qt)
+    f32 = dw.restore_f32().cpu().numpy()
+    want = orc.restore_matrix(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload)
+    assert np.array_equal(f32.view(np.uint32), want.view(np.uint32))
+    f16 = dw.restore_f16().cpu().view(torch.int16).numpy().view(np.uint16)
+    want16 = ref.restore_matrix_half(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload)
+    assert np.array_equal(f16, want16)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("shape", [(33, 200), (256, 256), (300, 1000), (1000, 4098)])
+@pytest.mark.parametrize("batch", [1, 2, 3, 5, 8, 9, 16, 17, 33])
+def test_linear_matches_reference_gemv(cuda, orc, sid, shape, batch):
+    rows, cols = shape
+    qt = quantized_gaussian(sid, rows, cols, seed=batch + rows)
+    x = gaussian_x(batch, cols, seed=batch)
+    dw = amsq.DeviceWeight(qt)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = dw.linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_linear_random_payload_large_k(cuda, orc, sid):
+    """Random valid payload (every code incl. -0 and subnormals) at K = 14336 (8B down)."""
+    rows, cols, batch = 256, 14336, 4
+    qt = random_payload(sid, rows, cols, seed=5)
+    x = gaussian_x(batch, cols, seed=9)
+    dw = amsq.DeviceWeight(qt)
+    y = dw.gemv_host(x, batch).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_subnormal_codes_survive_the_tensor_cores(cuda, orc, sid):
+    """Placed subnormal-source codes are binary16 subnormals; the MMA must not flush them."""
+    s = amsq.scheme_by_id(sid)
+    sub = [c for c in range(1, s.code_count // 2) if (c >> s.man_bits) == 0]  # exp field 0
+    rows, cols = 16, s.block * 64
+    codes = np.zeros(cols, np.uint8)
+    for i in range(0, cols, s.k):
+        codes[i:i + s.k] = sub[(i // s.k) % len(sub)] & ~1 | ((i // s.k) & 1)
+    codes = np.array([c if c != s.sign_mask else 0 for c in codes], np.uint8)
+    words = amsq.pack_row(codes, s)
+    qt = amsq.QuantizedTensor(s, rows, cols, cols, np.full(rows, 0x3C00, np.uint16),
+                              np.tile(words, rows))
+    x = np.full(cols, 0x3C00, np.uint16)  # ones
+    y = amsq.DeviceWeight(qt).gemv_host(x, 1)
+    want = sum(orc.decode(int(c), sid) for c in codes)
+    got = y.view(np.float16).astype(np.float64)
+    assert np.all(np.abs(got - want) <= 1e-3 * abs(want) + 1e-3), (got[:4], want)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_linear_deterministic_and_graph_replayable(cuda, sid):
+    rows, cols, batch = 4096, 4096, 8
+    qt = random_payload(sid, rows, cols, seed=1)
+    dw = amsq.DeviceWeight(qt)
+    x = torch.from_numpy(gaussian_x(batch, cols).view(np.float16).reshape(batch, cols)).to(cuda)
+    y0 = dw.linear(x).clone()
+    for _ in range(3):
+        assert torch.equal(dw.linear(x), y0)
+    out = torch.empty_like(y0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dw.linear(x, out=out, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        dw.linear(x, out=out)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, y0)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_upload_download_round_trip(cuda, sid):
+    for rows, cols in [(33, 200), (300, 4098), (1, 3)]:
+        qt = random_payload(sid, rows, cols, seed=rows)
+        back = amsq.DeviceWeight(qt).download()
+        assert np.array_equal(back.payload, qt.payload)
+        assert np.array_equal(back.scales, qt.scales)
+
+
+def test_shape_errors(cuda):
+    qt = quantized_gaussian(7, 4, 9)
+    dw = amsq.DeviceWeight(qt)
+    with pytest.raises(ValueError):
+        dw.gemv_host(np.zeros(7, np.uint16), 1)
+    with pytest.raises(ValueError):
+        dw.gemv_host(np.zeros(9, np.uint16), 0)
+    with pytest.raises(ValueError):
+        amsq.gemv(qt, np.zeros(8, np.uint16), 1)
+
+
+def test_reference_call_shapes(cuda, orc):
+    """amsq.gemv / restore_matrix with the reference signatures (host in, host out)."""
+    qt = quantized_gaussian(4, 70, 130, seed=2)
+    x = gaussian_x(3, 130)
+    y = amsq.gemv(qt, x, 3).reshape(3, 70)
+    yref = orc.gemv(4, 70, 130, qt.padded_cols, qt.scales, qt.payload, x, 3)
+    _, yabs = orc.gemv_f64(4, 70, 130, qt.padded_cols, qt.scales, qt.payload, x, 3)
+    check_linear(y, yref, yabs)
+    m = amsq.restore_matrix(qt)
+    want = orc.restore_matrix(4, 70, 130, qt.padded_cols, qt.scales, qt.payload)
+    assert np.array_equal(m.view(np.uint32), want.view(np.uint32))
