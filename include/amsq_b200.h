@@ -172,6 +172,12 @@ int amsq_tp_unshard(const uint16_t* d_gathered, size_t nranks, size_t batch, siz
 
 /* Number of this library's kernels launched so far in this process (bench accounting). */
 uint64_t amsq_kernel_launch_count(void);
+/* Profiling knob: when on, the fused linear streams its operands but skips decode/MMA
+ * (results are garbage). Used by tools/prof_linear.py to separate memory and compute. */
+void amsq_debug_set_dry_run(int on);
+/* Profiling knob: device buffer of >= 8 u64 per CTA receiving %globaltimer stamps
+ * (start, first stage landed, stream done, end) of each fused-linear CTA; NULL = off. */
+void amsq_debug_set_trace(void* d_buf);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,8 @@ SIGNATURES = {
     "amsq_linear_tp": (_I, [_P, _P, _SZ, _P, _P, _SZ, _P, _I, _P]),
     "amsq_tp_unshard": (_I, [_P, _SZ, _SZ, _SZ, _P, _P]),
     "amsq_kernel_launch_count": (C.c_uint64, []),
+    "amsq_debug_set_dry_run": (None, [_I]),
+    "amsq_debug_set_trace": (None, [_P]),
 }
 
 _lib = None

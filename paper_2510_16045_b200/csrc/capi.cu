@@ -30,6 +30,8 @@ struct amsq_weight_s {
 namespace {
 
 thread_local std::string g_error;
+int g_dry_run = 0;  // amsq_debug_set_dry_run(): profiling knob, never set by the product
+unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
 
 struct CudaError : std::runtime_error {
   cudaError_t code;
@@ -174,6 +176,8 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.ldy = static_cast<long long>(ldy);
   p.row_blocks = static_cast<int>(h->L.row_blocks());
   p.k_tiles = static_cast<int>(h->L.k_tiles);
+  p.dry = g_dry_run;
+  p.trace = g_trace;
   const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
   for (size_t b0 = 0; b0 < batch; b0 += step) {
     const size_t mb = batch - b0 < step ? batch - b0 : step;
@@ -509,5 +513,8 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
 }
 
 uint64_t amsq_kernel_launch_count(void) { return amsqb::kernel_launch_count(); }
+
+void amsq_debug_set_dry_run(int on) { g_dry_run = on; }
+void amsq_debug_set_trace(void* d_buf) { g_trace = static_cast<unsigned long long*>(d_buf); }
 
 }  // extern "C"

@@ -184,7 +184,7 @@ void repack_to_device(const DeviceLayout& L, const uint16_t* payload, uint8_t* o
   parallel_rows(L.row_tiles, threads, [&](size_t r0, size_t r1) {
     for (size_t rt = r0; rt < r1; ++rt) {
       for (size_t kt = 0; kt < L.k_tiles; ++kt) {
-        uint8_t* tile = out + (rt * L.k_tiles + kt) * L.tile_bytes;
+        uint8_t* tile = out + L.tile_offset(rt, kt);
         if (L.scheme_id == 4) {
           s4_pack_tile(L, payload, rt, kt, tile);
         } else {
@@ -199,7 +199,7 @@ void repack_from_device(const DeviceLayout& L, const uint8_t* in, uint16_t* payl
   parallel_rows(L.row_tiles, threads, [&](size_t r0, size_t r1) {
     for (size_t rt = r0; rt < r1; ++rt) {
       for (size_t kt = 0; kt < L.k_tiles; ++kt) {
-        const uint8_t* tile = in + (rt * L.k_tiles + kt) * L.tile_bytes;
+        const uint8_t* tile = in + L.tile_offset(rt, kt);
         if (L.scheme_id == 4) {
           s4_unpack_tile(L, tile, rt, kt, payload);
         } else {

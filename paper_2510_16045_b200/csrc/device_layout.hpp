@@ -25,9 +25,11 @@
 //      i=2: (mag4>>1)<<4, M1@13, sign@14 | high: (mag4>>1)<<20, M1@29, sign@30
 //      shared: a@12, b@28
 //
-// Tiles are stored [row_tile][k_tile] so one row tile's K range is one contiguous
-// run (a single cp.async.bulk per stage). Row tiles are padded to a multiple of 16
-// (256-row blocks), K to a multiple of TK; padding is zero and restores to +0.
+// Tiles are stored [row_block][k_tile][row_tile_in_block] (row block = 16 row tiles =
+// 256 rows): the 16 tiles of one k-tile are contiguous, so a pipeline stage of the fused
+// linear (one row block x kChunk k-tiles) is ONE cp.async.bulk of 16*kChunk tiles --
+// the TMA engine pays a fixed cost per copy, so copies must be large. Row tiles are
+// padded to a multiple of 16, K to a multiple of TK; padding is zero and restores to +0.
 #pragma once
 
 #include <cstddef>
@@ -45,6 +47,9 @@ struct DeviceLayout {
   size_t k_tiles = 0;
   size_t row_blocks() const { return row_tiles / 16; }
   size_t bytes() const { return row_tiles * k_tiles * tile_bytes; }
+  size_t tile_offset(size_t rt, size_t kt) const {
+    return ((rt / 16 * k_tiles + kt) * 16 + rt % 16) * tile_bytes;
+  }
 };
 
 constexpr size_t kRowsPerTile = 16;

@@ -3,10 +3,9 @@
 //  K1 amsq_restore_kernel   restore_block / restore_matrix(_half) over the tile layout
 //                           (kernels.hpp:55-133 of the reference), bit-exact.
 //  K2 amsq_linear_kernel    fused restore + linear for batch M <= 16 (kernels.hpp:151-187):
-//                           stream-K over (256-row block x k-tile) units, one persistent
-//                           CTA per SM, 8 warps x 2 row tiles, packed tiles streamed by the
-//                           TMA bulk engine into a per-warp mbarrier ring, decode in
-//                           registers, m16n8k16 tensor-core MMAs with fp32 accumulation,
+//                           warp-specialised persistent CTA per SM (TMA-bulk producer warp,
+//                           8 decode/MMA consumer warps), stream-K over (256-row block x
+//                           k-tile) units, m16n8k16 tensor-core MMAs with fp32 accumulation,
 //                           deterministic split-K fix-up (fixed order, no float atomics).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -39,7 +38,10 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
   const long long tile = static_cast<long long>(blockIdx.x) * 4 + warp;
   const long long ntiles = static_cast<long long>(p.row_tiles) * p.k_tiles;
   if (tile >= ntiles) return;
-  const int rt = static_cast<int>(tile / p.k_tiles), kt = static_cast<int>(tile % p.k_tiles);
+  // tiles are enumerated in storage order [row_block][k_tile][row_tile_in_block]
+  const long long rbk = tile / 16;
+  const int rt = static_cast<int>(rbk / p.k_tiles) * 16 + static_cast<int>(tile % 16);
+  const int kt = static_cast<int>(rbk % p.k_tiles);
   const uint8_t* src = p.w + tile * T::kTileBytes;
   const uint4 v = *reinterpret_cast<const uint4*>(src + lane * 16);
   const uint32_t R[4] = {v.x, v.y, v.z, v.w};
@@ -94,39 +96,59 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
 }
 
 // =====================================================================================
-// K2: fused restore + linear, M <= 8*NB.
+// K2: fused restore + linear, M <= 8*NB (NB = 1 or 2).
+//
+// Warp-specialised persistent CTA (one per SM): warp 8 is the producer -- its lane 0
+// streams, per pipeline stage, kChunk k-tiles of the CTA's 16 row tiles (one
+// cp.async.bulk per row tile) plus the matching activation rows (natural layout, one
+// bulk copy per batch row, zero-filled past `cols`) into a 4-deep ring guarded by
+// full/empty mbarriers. Warps 0..7 are consumers: warp w owns row tiles 2w, 2w+1,
+// decodes its 16 B per tile in registers, gathers B fragments with PRMT and issues
+// m16n8k16 MMAs (fp32 accumulation). Units are (256-row block, k-tile) pairs split
+// evenly over the grid (stream-K); a row block cut between CTAs is finished by the
+// last contributor, which sums the fp32 partials in CTA order (deterministic).
 // =====================================================================================
-constexpr int kWarps = 8;        // each warp: 2 row tiles = 32 rows; CTA: 256-row block
-constexpr int kChunk = 4;        // k-tiles per pipeline stage
-constexpr int kStages = 4;       // ring depth per warp
-constexpr int kXWin = 16;        // k-tiles of activations staged per window
+constexpr int kConsumerWarps = 8;
+constexpr int kK2Threads = (kConsumerWarps + 1) * 32;
+constexpr int kChunk = 2;    // k-tiles per stage
+constexpr int kStages = 5;   // ring depth (two CTAs per SM share the 227 KB)
+constexpr int kCtasPerSM = 2;
 
 template <int SCHEME, int NB>
-struct K2Smem {
+struct K2Layout {
   using T = Traits<SCHEME>;
   static constexpr int kMS = 8 * NB;
-  static constexpr int kStageBytes = 2 * kChunk * T::kTileBytes;
-  static constexpr int kRingBytes = kWarps * kStages * kStageBytes;
-  static constexpr int kXsBytes = kXWin * T::kJ * kMS * 4 * 8;
-  static constexpr int kBarOff = kRingBytes + kXsBytes;
-  static constexpr int kBytes = kBarOff + kWarps * kStages * 8 + 16;
+  static constexpr int kWBytes = 16 * kChunk * T::kTileBytes;
+  // activation row stride padded so the lanes' LDS hit distinct banks:
+  // stride = 96 (mod 128) bytes for the 24-byte FP5.33 lane runs, 16 (mod 128) for FP4.25
+  static constexpr int kXRaw = kChunk * T::kTK * 2;
+  static constexpr int kXTarget = SCHEME == 7 ? 96 : 16;
+  static constexpr int kXRow = kXRaw + ((kXTarget - kXRaw % 128) + 128) % 128;
+  static constexpr int kStageBytes = kWBytes + kMS * kXRow;
+  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kBytes = kBarOff + 2 * kStages * 8 + 16;
+  static_assert(kWBytes % 16 == 0 && kXRow % 16 == 0 && kStageBytes % 16 == 0, "alignment");
 };
 
-// Walks the CTA's unit range [u, u1) in chunks that never cross a row block.
+// Walks a CTA's unit range [u, u1) in chunks that never cross a row block.
 struct ChunkIter {
   long long u, u1;
-  int KT;
+  int rb, kt, KT;
+  __device__ ChunkIter(long long u0, long long u1_, int KT_) : u(u0), u1(u1_), KT(KT_) {
+    rb = static_cast<int>(u0 / KT_);
+    kt = static_cast<int>(u0 - static_cast<long long>(rb) * KT_);
+  }
   __device__ bool valid() const { return u < u1; }
-  __device__ void get(int& rb, int& kt, int& nk) const {
-    rb = static_cast<int>(u / KT);
-    kt = static_cast<int>(u - static_cast<long long>(rb) * KT);
-    const long long seg_end = min(u1, static_cast<long long>(rb + 1) * KT);
-    nk = static_cast<int>(min(static_cast<long long>(kChunk), seg_end - u));
+  __device__ int nk() const {
+    const long long left = u1 - u;
+    int n = KT - kt < kChunk ? KT - kt : kChunk;
+    return left < n ? static_cast<int>(left) : n;
   }
   __device__ void next() {
-    int rb, kt, nk;
-    get(rb, kt, nk);
-    u += nk;
+    const int n = nk();
+    u += n;
+    kt += n;
+    if (kt == KT) kt = 0, ++rb;
   }
 };
 
@@ -138,60 +160,135 @@ __device__ __forceinline__ long long unit_owner(long long u, long long U, long l
   return ((u + 1) * G - 1) / U;
 }
 
+// One k-tile of the consumer loop for a warp's two row tiles: decode, gather the B
+// fragments of every batch block from the natural-layout activations, 2*J*NB MMAs.
 template <int SCHEME, int NB>
-__global__ void __launch_bounds__(kWarps * 32, 1) amsq_linear_kernel(LinearParams p) {
+__device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const uint4 (&wv)[2],
+                                              const uint32_t (&sh)[2], float (&acc)[2][NB][4],
+                                              int g, int t, int M) {
   using T = Traits<SCHEME>;
-  using SM = K2Smem<SCHEME, NB>;
+  using LY = K2Layout<SCHEME, NB>;
   constexpr int J = T::kJ;
-  constexpr int MS = SM::kMS;
+  uint32_t A[2][J][4];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const uint32_t R[4] = {wv[rr].x, wv[rr].y, wv[rr].z, wv[rr].w};
+    if constexpr (SCHEME == 4) {
+      decode_s4(R, sh[rr], A[rr]);
+    } else {
+      decode_s7(R, A[rr]);
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const int m = nb * 8 + g;
+    const uint8_t* xp = st + LY::kWBytes + m * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
+    uint32_t B[J][2];
+    if constexpr (SCHEME == 4) {
+      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (m < M) {
+        const uint4 a = *reinterpret_cast<const uint4*>(xp);
+        const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
+        w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w;
+        w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+      }
+      bfrag_s4(w, B);
+    } else {
+      uint32_t w[6] = {0, 0, 0, 0, 0, 0};
+      if (m < M) {
+        const uint2 a = *reinterpret_cast<const uint2*>(xp);
+        const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
+        const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
+        w[0] = a.x, w[1] = a.y, w[2] = b.x, w[3] = b.y, w[4] = d.x, w[5] = d.y;
+      }
+      bfrag_s7(w, B);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      mma16816(acc[0][nb], A[0][j], B[j][0], B[j][1]);
+      mma16816(acc[1][nb], A[1][j], B[j][0], B[j][1]);
+    }
+  }
+}
+
+template <int SCHEME, int NB>
+__global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(LinearParams p) {
+  using T = Traits<SCHEME>;
+  using LY = K2Layout<SCHEME, NB>;
+  constexpr int J = T::kJ;
+  constexpr int TILE = T::kTileBytes;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  uint2* xs = reinterpret_cast<uint2*>(smem + SM::kRingBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBarOff);
-  int* flag = reinterpret_cast<int*>(smem + SM::kBarOff + kWarps * kStages * 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff);
+  uint64_t* empty = full + kStages;
+  int* flag = reinterpret_cast<int*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
   const long long U = static_cast<long long>(p.row_blocks) * p.k_tiles;
   const long long G = gridDim.x;
   const long long c = blockIdx.x;
   const long long u0 = unit_start(c, U, G), u1 = unit_start(c + 1, U, G);
   const int KT = p.k_tiles;
+  unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
-  uint64_t* mybars = bars + warp * kStages;
-  uint8_t* myring = ring + warp * kStages * SM::kStageBytes;
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&mybars[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1 + 32);  // expect_tx arrival + one per producer lane
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     fence_barrier_init();
   }
-  __syncwarp();
-  const uint64_t pol = policy_evict_first();
+  __syncthreads();
 
-  // producer: lane 0 streams this warp's two row tiles of each chunk
-  auto issue = [&](const ChunkIter& it, int stage) {
-    int rb, kt, nk;
-    it.get(rb, kt, nk);
-    const int rt0 = rb * 16 + 2 * warp;
-    const uint32_t bytes = static_cast<uint32_t>(nk * T::kTileBytes);
-    uint8_t* dst = myring + stage * SM::kStageBytes;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&mybars[stage], 2 * bytes);
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const uint8_t* src =
-          p.w + (static_cast<long long>(rt0 + rr) * KT + kt) * static_cast<long long>(T::kTileBytes);
-      bulk_g2s(dst + rr * kChunk * T::kTileBytes, src, bytes, &mybars[stage], pol);
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer warp
+    // lane 0: one bulk copy of the stage's 16*nk weight tiles (contiguous in the
+    // [row_block][k_tile][row_tile] layout); all lanes: the activation rows with 16-byte
+    // LDGSTS (zero-filled past `cols`), each lane arriving once on the full barrier.
+    const uint64_t pol = policy_evict_first();
+    const bool x_vec = ((p.cols & 7) == 0) && ((p.ldx & 7) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
+    constexpr int kXUnits = kChunk * T::kTK * 2 / 16;  // 16-byte units per activation row
+    ChunkIter it(u0, u1, KT);
+    for (int i = 0; it.valid(); ++i, it.next()) {
+      const int s = i % kStages;
+      if (i >= kStages) mbar_wait(&empty[s], static_cast<uint32_t>((i / kStages) - 1) & 1u);
+      const int nk = it.nk();
+      uint8_t* st = smem + s * LY::kStageBytes;
+      const long long k0 = static_cast<long long>(it.kt) * T::kTK;
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
+        mbar_arrive_expect_tx(&full[s], wbytes);
+        bulk_g2s(st, p.w + (static_cast<long long>(it.rb) * KT + it.kt) * 16LL * TILE, wbytes,
+                 &full[s], pol);
+      }
+      const int units = p.M * kXUnits;
+      if (x_vec) {
+        for (int u = lane; u < units; u += 32) {
+          const int m = u / kXUnits, q = u - m * kXUnits;
+          const long long k = k0 + q * 8;
+          const long long left = p.cols - k;
+          const uint32_t nbytes = left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
+          const unsigned short* src = p.x + m * p.ldx + (nbytes ? k : 0);
+          cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16, src, nbytes);
+        }
+        cp_async_mbar_arrive(&full[s]);
+      } else {  // unaligned activations: plain loads, then a regular arrival
+        for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
+          const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
+          unsigned short* xr = reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
+          xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e) : static_cast<unsigned short>(0);
+        }
+        __threadfence_block();
+        mbar_arrive(&full[s]);
+      }
     }
-  };
-
-  ChunkIter prod{u0, u1, KT}, cons{u0, u1, KT};
-  if (lane == 0) {
-    for (int s = 0; s < kStages && prod.valid(); ++s) {
-      issue(prod, s);
-      prod.next();
-    }
+    return;
   }
 
+  // -------------------------------------------------------------- consumer warps
+  const int g = lane >> 2, t = lane & 3;
   float acc[2][NB][4];
   auto zero_acc = [&] {
 #pragma unroll
@@ -202,51 +299,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) amsq_linear_kernel(LinearParam
         for (int e = 0; e < 4; ++e) acc[rr][nb][e] = 0.0f;
   };
   zero_acc();
-
-  int stage = 0;
-  uint32_t phase = 0;
   int cur_rb = -1, seg_kt0 = 0, seg_kt1 = 0;
-  int xw_lo = 0, xw_hi = 0;  // staged activation window [lo, hi) in k-tiles
+  constexpr int kCons = kConsumerWarps * 32;
 
-  // Stage x[:, xw_lo*TK .. xw_hi*TK) permuted into the B-fragment order, zero padded.
-  auto stage_x = [&](int lo) {
-    __syncthreads();
-    xw_lo = lo;
-    xw_hi = min(lo + kXWin, KT);
-    const int nkt = xw_hi - xw_lo;
-    const int nunits = nkt * MS * 4;  // (ktl, m, t): one lane chunk of TK/4 columns
-    for (int idx = threadIdx.x; idx < nunits; idx += blockDim.x) {
-      const int tt = idx & 3;
-      const int m = (idx >> 2) % MS;
-      const int ktl = (idx >> 2) / MS;
-      const long long kbase = static_cast<long long>(xw_lo + ktl) * T::kTK + tt * T::kLaneK;
-      __half v[T::kLaneK];
-      const bool live = m < p.M;
-      const unsigned short* xr = p.x + static_cast<long long>(m) * p.ldx;
-#pragma unroll
-      for (int e = 0; e < T::kLaneK; ++e) {
-        const long long k = kbase + e;
-        v[e] = (live && k < p.cols) ? __ushort_as_half(__ldg(xr + k)) : __ushort_as_half(0);
-      }
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        __half2 lo2 = __halves2half2(v[T::kofs(j, 0)], v[T::kofs(j, 1)]);
-        __half2 hi2 = __halves2half2(v[T::kofs(j, 2)], v[T::kofs(j, 3)]);
-        uint2 u;
-        u.x = *reinterpret_cast<uint32_t*>(&lo2);
-        u.y = *reinterpret_cast<uint32_t*>(&hi2);
-        xs[((ktl * J + j) * MS + m) * 4 + tt] = u;
-      }
-    }
-    __syncthreads();
-  };
-
-  // End of a row-block segment: direct store when this CTA covered the whole K range,
-  // otherwise publish a partial and let the last contributor reduce in CTA order.
   auto finish_segment = [&](int rb) {
-    const bool full = (seg_kt0 == 0 && seg_kt1 == KT);
-    const int rib0 = 32 * warp;  // row-in-block of this warp's first row tile
-    if (full) {
+    const int rib0 = 32 * warp;
+    if (seg_kt0 == 0 && seg_kt1 == KT) {  // this CTA covered the whole K range
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
@@ -269,6 +327,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) amsq_linear_kernel(LinearParam
       }
       return;
     }
+    constexpr int MS = 8 * NB;
     const long long pid = c + rb;
     float* part = p.partials + pid * MS * 256;
 #pragma unroll
@@ -282,87 +341,105 @@ __global__ void __launch_bounds__(kWarps * 32, 1) amsq_linear_kernel(LinearParam
             const int m = nb * 8 + 2 * t + e;
             part[m * 256 + rib0 + rr * 16 + g + 8 * h] = acc[rr][nb][2 * h + e];
           }
-    __threadfence();
-    __syncthreads();
+    named_bar_sync(1, kCons);  // all partial stores of this CTA happen-before thread 0's ticket
     const long long c_first = unit_owner(static_cast<long long>(rb) * KT, U, G);
     const long long c_last = unit_owner(static_cast<long long>(rb + 1) * KT - 1, U, G);
     if (threadIdx.x == 0) {
       const int ncontrib = static_cast<int>(c_last - c_first + 1);
-      const int old = atomicAdd(&p.counters[rb], 1);
+      const int old = atomic_add_acq_rel_gpu(&p.counters[rb], 1);
       const int last = (old == ncontrib - 1);
-      if (last) {
-        __threadfence();
-        p.counters[rb] = 0;  // self-cleaning for the next launch / graph replay
-      }
+      if (last) store_relaxed_gpu(&p.counters[rb], 0);  // self-cleaning for the next launch
       *flag = last;
     }
-    __syncthreads();
+    named_bar_sync(1, kCons);
     if (*flag) {
-      for (int idx = threadIdx.x; idx < p.M * 256; idx += blockDim.x) {
-        const int m = idx >> 8, rib = idx & 255;
-        const long long n = static_cast<long long>(rb) * 256 + rib;
-        if (n >= p.rows) continue;
-        float s = 0.0f;
-        for (long long cc = c_first; cc <= c_last; ++cc) {
-          s += __ldcg(p.partials + ((cc + rb) * MS + m) * 256 + rib);
+      // Sum the contributors' partials in CTA order (deterministic). All loads of a batch
+      // are issued before any add so the L2 latency is paid once per batch, not per term.
+      const int ncon = static_cast<int>(c_last - c_first + 1);
+      const float4* base = reinterpret_cast<const float4*>(p.partials + (c_first + rb) * MS * 256);
+      constexpr int kB = 8;
+      for (int o = threadIdx.x; o < p.M * 64; o += kCons) {
+        const int m = o >> 6, q = o & 63;
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c0 = 0; c0 < ncon; c0 += kB) {
+          float4 v[kB];
+#pragma unroll
+          for (int j = 0; j < kB; ++j) {
+            v[j] = (c0 + j < ncon) ? __ldcg(base + ((c0 + j) * MS + m) * 64 + q)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int j = 0; j < kB; ++j) {
+            if (c0 + j < ncon) {
+              sum.x += v[j].x, sum.y += v[j].y, sum.z += v[j].z, sum.w += v[j].w;
+            }
+          }
         }
-        const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
-        p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(s * sc));
+        const float r4[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long n = static_cast<long long>(rb) * 256 + 4 * q + e;
+          if (n < p.rows) {
+            const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+            p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(r4[e] * sc));
+          }
+        }
       }
     }
-    __syncthreads();
+    named_bar_sync(1, kCons);
   };
 
-  while (cons.valid()) {
-    int rb, kt, nk;
-    cons.get(rb, kt, nk);
-    if (rb != cur_rb) {
+  ChunkIter it(u0, u1, KT);
+  for (int i = 0; it.valid(); ++i, it.next()) {
+    const int s = i % kStages;
+    const int nk = it.nk();
+    if (it.rb != cur_rb) {
       if (cur_rb >= 0) finish_segment(cur_rb);
       zero_acc();
-      cur_rb = rb;
-      seg_kt0 = kt;
+      cur_rb = it.rb;
+      seg_kt0 = it.kt;
     }
-    seg_kt1 = kt + nk;
-    if (kt < xw_lo || kt + nk > xw_hi) stage_x(kt);
-
-    mbar_wait(&mybars[stage], phase);
-    const uint8_t* sbase = myring + stage * SM::kStageBytes;
-    for (int kk = 0; kk < nk; ++kk) {
-      uint32_t A[2][J][4];
+    seg_kt1 = it.kt + nk;
+    mbar_wait(&full[s], static_cast<uint32_t>(i / kStages) & 1u);
+    if (trace && i == 0 && threadIdx.x == 0) trace[1] = globaltimer();
+    const uint8_t* st = smem + s * LY::kStageBytes;
+    const uint8_t* wt = st + (2 * warp) * TILE + lane * 16;  // stage: [kk][16 row tiles]
+    if (p.dry) {
+      // profiling mode: stream only
+    } else if (nk == kChunk) {
+      // common case: guard-free, fully unrolled so loads of later k-tiles overlap the
+      // decode/MMA of earlier ones
+      uint4 wv[kChunk][2];
+      uint32_t sh[kChunk][2];
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const uint8_t* tp = sbase + (rr * kChunk + kk) * T::kTileBytes;
-        const uint4 v = *reinterpret_cast<const uint4*>(tp + lane * 16);
-        const uint32_t R[4] = {v.x, v.y, v.z, v.w};
-        if constexpr (SCHEME == 4) {
-          decode_s4(R, tp[512 + lane], A[rr]);
-        } else {
-          decode_s7(R, A[rr]);
+      for (int kk = 0; kk < kChunk; ++kk)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
+          wv[kk][rr] = *reinterpret_cast<const uint4*>(tp);
+          sh[kk][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
         }
-      }
-      const int ktl = kt + kk - xw_lo;
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
+      for (int kk = 0; kk < kChunk; ++kk) consume_ktile<SCHEME, NB>(st, kk, wv[kk], sh[kk], acc, g, t, p.M);
+    } else {
+      for (int kk = 0; kk < nk; ++kk) {
+        uint4 wv[2];
+        uint32_t sh[2];
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const uint2 b = xs[((ktl * J + j) * MS + nb * 8 + g) * 4 + t];
-          mma16816(acc[0][nb], A[0][j], b.x, b.y);
-          mma16816(acc[1][nb], A[1][j], b.x, b.y);
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
+          wv[rr] = *reinterpret_cast<const uint4*>(tp);
+          sh[rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
         }
+        consume_ktile<SCHEME, NB>(st, kk, wv, sh, acc, g, t, p.M);
       }
     }
     __syncwarp();
-    if (lane == 0 && prod.valid()) {
-      issue(prod, stage);
-      prod.next();
-    }
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1u;
-    }
-    cons.next();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if (trace && threadIdx.x == 0) trace[2] = globaltimer();
   if (cur_rb >= 0) finish_segment(cur_rb);
+  if (trace && threadIdx.x == 0) trace[3] = globaltimer();
 }
 
 }  // namespace dev
@@ -385,7 +462,7 @@ cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s) {
 
 template <int SCHEME, int NB>
 static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t s) {
-  using SM = dev::K2Smem<SCHEME, NB>;
+  using SM = dev::K2Layout<SCHEME, NB>;
   static bool configured = false;  // per template instance; attribute is per-function
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB>,
@@ -393,7 +470,7 @@ static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dev::amsq_linear_kernel<SCHEME, NB><<<grid, dev::kWarps * 32, SM::kBytes, s>>>(p);
+  dev::amsq_linear_kernel<SCHEME, NB><<<grid, dev::kK2Threads, SM::kBytes, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

@@ -9,7 +9,7 @@ namespace amsqb {
 
 // Fixed persistent grid of the stream-K linear: the split-K partition (and therefore the
 // fp32 reduction order) depends only on the shape, never on the device it runs on.
-constexpr long long kGridCTAs = 148;
+constexpr long long kGridCTAs = 2 * 148;  // two CTAs per SM on the 148-SM B200
 
 struct RestoreParams {
   int scheme_id;
@@ -33,6 +33,8 @@ struct LinearParams {
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
   int row_blocks, k_tiles;
+  int dry;                  // profiling only: consumers skip decode/MMA (measures the stream)
+  unsigned long long* trace;  // profiling only: per-CTA globaltimer stamps (null = off)
 };
 
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);

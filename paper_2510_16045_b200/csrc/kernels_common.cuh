@@ -76,6 +76,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Named barrier among `nthreads` threads (the consumer warps of a warp-specialised CTA).
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Ticket for the split-K fix-up: acq_rel at gpu scope orders this CTA's partial stores
+// (published to thread 0 by the preceding bar.sync) before the increment, and makes the
+// other contributors' partials visible to the last arriver.
+__device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void store_relaxed_gpu(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -92,6 +127,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// LDGSTS: 16-byte async global -> shared copy; bytes past `src_bytes` are zero-filled.
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+// One arrival on `bar` once all of this thread's prior cp.async have landed (the
+// barrier's expected count must include it: .noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 // D[16x8,f32] += A[16x16,f16,row] * B[16x8,f16,col]
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
@@ -103,21 +152,42 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 }
 
 // ------------------------------------------------------------------ decode
+// Explicit LOP3s: (a & b) | c in one ALU op (0xEA), a & b (0x80). Shifts are written as
+// multiplies / mul.hi so ptxas can issue them on the FMA pipe (IMAD / IMAD.HI), keeping
+// the ALU pipe -- the decode's bottleneck -- for the masks.
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t and2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, 0, 0xC0;" : "=r"(d) : "r"(a), "r"(b));  // a & b
+  return d;
+}
+__device__ __forceinline__ uint32_t imul(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 // FP4.25: R[0..3] (see device_layout.hpp), sh = the lane's shared byte.
 // Output A[j] = the four A-fragment registers of MMA j:
 //   {row g pair (k 16t+j, 16t+4+j), row g+8 same, row g (16t+8+j, 16t+12+j), row g+8 same}
+// Per register: 7 ALU (LOP3) + 4 FMA-pipe (IMAD) ops for 8 weights.
 __device__ __forceinline__ void decode_s4(const uint32_t (&R)[4], uint32_t sh,
                                           uint32_t (&A)[4][4]) {
-  const uint32_t T = sh * 0x1001u;  // sh | sh << 12: bit q -> q, bit q+4 -> q+16
+  const uint32_t T = imul(sh, 0x1001u);  // sh | sh << 12: bit q -> q, bit q+4 -> q+16
   uint32_t o[4][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t S = (T << (8 - q)) & 0x01000100u;  // shared LSBs of groups a, b -> bits 8, 24
+    // shared LSBs of groups a, b -> bits 8, 24
+    const uint32_t S = and2(imul(T, 1u << (8 - q)), 0x01000100u);
     const uint32_t r = R[q];
-    o[q][0] = (r & 0x8E008E00u) | S;
-    o[q][1] = ((r << 3) & 0x8E008E00u) | S;
-    o[q][2] = (((r & 0x20382038u) * 68u) & 0x8E008E00u) | S;   // mag <<6, sign <<2
-    o[q][3] = (((r & 0x40074007u) * 514u) & 0x8E008E00u) | S;  // mag <<9, sign <<1
+    o[q][0] = and_or(r, 0x8E008E00u, S);
+    o[q][1] = and_or(imul(r, 8u), 0x8E008E00u, S);
+    o[q][2] = and_or(imul(and2(r, 0x20382038u), 68u), 0x8E008E00u, S);   // mag <<6, sign <<2
+    o[q][3] = and_or(imul(and2(r, 0x40074007u), 514u), 0x8E008E00u, S);  // mag <<9, sign <<1
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -130,17 +200,18 @@ __device__ __forceinline__ void decode_s4(const uint32_t (&R)[4], uint32_t sh,
 
 // FP5.33: A[j] for MMA j in {0,1,2}; row-g outputs in order
 // [R0.o0, R0.o1, R0.o2, R1.o0, R1.o1, R1.o2], MMA j takes entries 2j, 2j+1.
+// Per register: 6 ALU + 3 FMA-pipe ops for 6 weights.
 __device__ __forceinline__ void decode_s7(const uint32_t (&R)[4], uint32_t (&A)[3][4]) {
   uint32_t o[4][3];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t r = R[q];
-    const uint32_t t5 = r >> 5;
-    const uint32_t S = t5 & 0x00800080u;     // shared bits 12/28 -> 7/23
-    const uint32_t SM1 = t5 & 0x01800180u;   // + member-2 M1 13/29 -> 8/24
-    o[q][0] = (r & 0x8F008F00u) | S;
-    o[q][1] = ((r << 8) & 0x8F008F00u) | S;
-    o[q][2] = (((r & 0x40704070u) * 34u) & 0x8E008E00u) | SM1;  // mag-hi <<5, sign <<1
+    const uint32_t t5 = __umulhi(r, 1u << 27);  // r >> 5 on the FMA pipe
+    const uint32_t S = and2(t5, 0x00800080u);     // shared bits 12/28 -> 7/23
+    const uint32_t SM1 = and2(t5, 0x01800180u);   // + member-2 M1 13/29 -> 8/24
+    o[q][0] = and_or(r, 0x8F008F00u, S);
+    o[q][1] = and_or(imul(r, 256u), 0x8F008F00u, S);
+    o[q][2] = and_or(imul(and2(r, 0x40704070u), 34u), 0x8E008E00u, SM1);  // mag-hi <<5, sign <<1
   }
   const uint32_t g0[6] = {o[0][0], o[0][1], o[0][2], o[1][0], o[1][1], o[1][2]};
   const uint32_t g8[6] = {o[2][0], o[2][1], o[2][2], o[3][0], o[3][1], o[3][2]};
@@ -151,6 +222,30 @@ __device__ __forceinline__ void decode_s7(const uint32_t (&R)[4], uint32_t (&A)[
     A[j][2] = g0[2 * j + 1];
     A[j][3] = g8[2 * j + 1];
   }
+}
+
+// ------------------------------------------------------------------ B fragments
+// The lane (g, t) holds its LK contiguous activation columns of row g as 16-bit pairs
+// w[i] = (x[2i], x[2i+1]); PRMT gathers the pairs each MMA's B slots name
+// (Traits::kofs), so x can stay in its natural layout in shared memory.
+__device__ __forceinline__ void bfrag_s7(const uint32_t (&w)[6], uint32_t (&B)[3][2]) {
+  B[0][0] = prmt(w[0], w[1], 0x7610);  // (x0, x3)
+  B[0][1] = prmt(w[0], w[2], 0x5432);  // (x1, x4)
+  B[1][0] = prmt(w[1], w[2], 0x7610);  // (x2, x5)
+  B[1][1] = prmt(w[3], w[4], 0x7610);  // (x6, x9)
+  B[2][0] = prmt(w[3], w[5], 0x5432);  // (x7, x10)
+  B[2][1] = prmt(w[4], w[5], 0x7610);  // (x8, x11)
+}
+
+__device__ __forceinline__ void bfrag_s4(const uint32_t (&w)[8], uint32_t (&B)[4][2]) {
+  B[0][0] = prmt(w[0], w[2], 0x5410);  // (x0, x4)
+  B[0][1] = prmt(w[4], w[6], 0x5410);  // (x8, x12)
+  B[1][0] = prmt(w[0], w[2], 0x7632);  // (x1, x5)
+  B[1][1] = prmt(w[4], w[6], 0x7632);  // (x9, x13)
+  B[2][0] = prmt(w[1], w[3], 0x5410);  // (x2, x6)
+  B[2][1] = prmt(w[5], w[7], 0x5410);  // (x10, x14)
+  B[3][0] = prmt(w[1], w[3], 0x7632);  // (x3, x7)
+  B[3][1] = prmt(w[5], w[7], 0x7632);  // (x11, x15)
 }
 
 }  // namespace dev

@@ -71,7 +71,9 @@ def placed_matrix(scheme: int, tiles: np.ndarray, row_tiles: int, k_tiles: int) 
     with every A-fragment element put at the column its B-fragment partner selects."""
     tr = TRAITS[scheme]
     tb, TK, J, LK = tr["tile_bytes"], tr["tk"], tr["J"], tr["lane_k"]
-    t = tiles.reshape(row_tiles, k_tiles, tb)
+    # storage order [row_block][k_tile][row_tile_in_block] (device_layout.hpp)
+    t = tiles.reshape(row_tiles // 16, k_tiles, 16, tb).transpose(0, 2, 1, 3).reshape(
+        row_tiles, k_tiles, tb)
     R = t[:, :, :512].copy().view(np.uint32).reshape(row_tiles, k_tiles, 32, 4)
     if scheme == 4:
         A = decode_s4(R, t[:, :, 512:544].astype(U32))
