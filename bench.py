@@ -163,61 +163,88 @@ def run_ours(args, world, rank, local):
           for name, (n, k) in shapes.items() for m in batches}
     calls = [(name, m) for m in batches for name in shapes]
     stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
 
-    def step(i, ev=None):
-        ws = sets[i % copies]
-        for ci, (name, m) in enumerate(calls):
-            if ev is not None:
-                ev[ci][0].record(stream)
-            rc = lib().amsq_linear(ws[name].handle, xs[(name, m)].data_ptr(), m,
-                                   ys[(name, m)].data_ptr(), sp)
-            if rc:
-                raise RuntimeError(lib().amsq_last_error().decode())
-            if ev is not None:
-                ev[ci][1].record(stream)
+    def launch(ws, name, m, st):
+        rc = lib().amsq_linear(ws[name].handle, xs[(name, m)].data_ptr(), m,
+                               ys[(name, m)].data_ptr(), st)
+        if rc:
+            raise RuntimeError(lib().amsq_last_error().decode())
+
+    # One step = the 16 calls, captured once per weight copy as a CUDA graph (the decode
+    # step of a serving stack is graph-launched; launches are PDL-chained inside).
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    graphs = []
+    with torch.cuda.stream(cap):
+        for c in range(copies):  # warm the per-function attributes outside capture
+            for name, m in calls:
+                launch(sets[c], name, m, cap.cuda_stream)
+        cap.synchronize()
+        per_step = None
+        for c in range(copies):
+            g = torch.cuda.CUDAGraph()
+            l0 = amsq.kernel_launch_count()
+            with torch.cuda.graph(g, stream=cap):
+                for name, m in calls:
+                    launch(sets[c], name, m, cap.cuda_stream)
+            per_step = amsq.kernel_launch_count() - l0
+            graphs.append(g)
+    stream.wait_stream(cap)
 
     for i in range(args.warmup):
-        step(i)
+        graphs[i % copies].replay()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-            for _ in calls] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = amsq.kernel_launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(args.steps):
-            step(i, evs[i])
+            graphs[i % copies].replay()
         t1.record(stream)
         torch.cuda.synchronize()
-    launches = amsq.kernel_launch_count() - launches0
+    launches = per_step * args.steps
     total_ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(tt.item())
-    per_call = {c: [evs[i][ci][0].elapsed_time(evs[i][ci][1]) for i in range(args.steps)]
-                for ci, c in enumerate(calls)}
     bytes_per_step = sum(payload_bytes[name] for name, m in calls)
     value = world * bytes_per_step * args.steps / (total_ms * 1e-3) / 1e9
 
-    # --- cuBLAS FP16 baseline on the same shapes/rotation (F.linear -> cublasGemmEx)
+    # Per-call device time: a graph of R back-to-back calls of one (shape, M), weights
+    # rotating over the copies, replayed; same for cuBLAS FP16 (F.linear -> cublasGemmEx).
+    R = 4 * copies
     dense = [{name: torch.randn(n, k, device=dev).half() for name, (n, k) in shapes.items()}
-             for _ in range(2)]
-    cub = {}
-    for name, m in calls:
-        ts = []
-        for i in range(args.warmup + args.steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            F.linear(xs[(name, m)], dense[i % 2][name])
-            b.record(stream)
-            ts.append((a, b))
+             for _ in range(copies)]
+
+    def graph_time(fn):
+        with torch.cuda.stream(cap):
+            fn(0)
+            cap.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                for r in range(R):
+                    fn(r)
+        stream.wait_stream(cap)
+        g.replay()
         torch.cuda.synchronize()
-        cub[(name, m)] = [a.elapsed_time(b) for a, b in ts[args.warmup:]]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, args.steps)
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3 / (reps * R)
+
+    per_call, cub = {}, {}
+    for name, m in calls:
+        per_call[(name, m)] = graph_time(
+            lambda r, name=name, m=m: launch(sets[r % copies], name, m, cap.cuda_stream))
+        cub[(name, m)] = graph_time(
+            lambda r, name=name, m=m: F.linear(xs[(name, m)], dense[r % copies][name]))
     del dense
     torch.cuda.empty_cache()
 
@@ -226,11 +253,11 @@ def run_ours(args, world, rank, local):
     alg_total, t_total = 0.0, 0.0
     for name, m in calls:
         n, k = shapes[name]
-        us = statistics.median(per_call[(name, m)]) * 1e3
-        cub_us = statistics.median(cub[(name, m)]) * 1e3
+        us = per_call[(name, m)]
+        cub_us = cub[(name, m)]
         alg = algorithmic_bytes(payload_bytes[name], n, k, m)
-        alg_total += alg * args.steps
-        t_total += sum(per_call[(name, m)]) * 1e-3
+        alg_total += alg
+        t_total += us * 1e-6
         detail.append({"layer": name, "N": n, "K": k, "M": m, "us": round(us, 2),
                        "packed_GBps": round(payload_bytes[name] / us / 1e3, 1),
                        "alg_GBps": round(alg / us / 1e3, 1),
@@ -270,6 +297,8 @@ def run_ours(args, world, rank, local):
                      "kernel": "amsq_linear_kernel", "peak_kind": peak_kind,
                      "bytes": "algorithmic = packed_payload_bytes + 2N + 2MK + 2MN per call"},
         "gpu_launches": int(launches),
+        "timing": "device time of CUDA-graph replays (16 PDL-chained calls per step); per-call "
+                  "detail from graphs of back-to-back calls of one shape",
         "clocks": clk.summary(),
         "detail": detail,
     }

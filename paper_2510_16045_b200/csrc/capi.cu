@@ -139,10 +139,10 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");
   ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
   ck(cudaMalloc(&h->d_partials, partial_floats * sizeof(float)), "cudaMalloc(partials)");
-  ck(cudaMalloc(&h->d_counters, h->L.row_blocks() * sizeof(int)), "cudaMalloc(counters)");
+  ck(cudaMalloc(&h->d_counters, h->L.row_blocks() * 8 * sizeof(int)), "cudaMalloc(counters)");
   ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
   ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
-  ck(cudaMemsetAsync(h->d_counters, 0, h->L.row_blocks() * sizeof(int), st), "memset counters");
+  ck(cudaMemsetAsync(h->d_counters, 0, h->L.row_blocks() * 8 * sizeof(int), st), "memset counters");
   ck(cudaStreamSynchronize(st), "upload sync");  // host staging buffers die here
   return h.release();
 }

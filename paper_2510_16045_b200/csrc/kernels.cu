@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
 // =====================================================================================
 constexpr int kConsumerWarps = 8;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;
-constexpr int kChunk = 2;    // k-tiles per stage
-constexpr int kStages = 5;   // ring depth (two CTAs per SM share the 227 KB)
+constexpr int kChunk = 3;    // k-tiles per stage: 24-26 KB bulk copies (>= 16 KB, tools/tma_probe.cu)
+constexpr int kStages = 3;   // ring depth (two CTAs per SM share the 228 KB)
 constexpr int kCtasPerSM = 2;
 
 template <int SCHEME, int NB>
@@ -128,44 +128,35 @@ struct K2Layout {
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kBytes = kBarOff + 2 * kStages * 8 + 16;
   static_assert(kWBytes % 16 == 0 && kXRow % 16 == 0 && kStageBytes % 16 == 0, "alignment");
+  static_assert(kBytes <= 113 * 1024, "two CTAs per SM must fit in shared memory");
 };
 
-// Walks a CTA's unit range [u, u1) in chunks that never cross a row block.
-struct ChunkIter {
-  long long u, u1;
-  int rb, kt, KT;
-  __device__ ChunkIter(long long u0, long long u1_, int KT_) : u(u0), u1(u1_), KT(KT_) {
-    rb = static_cast<int>(u0 / KT_);
-    kt = static_cast<int>(u0 - static_cast<long long>(rb) * KT_);
-  }
-  __device__ bool valid() const { return u < u1; }
-  __device__ int nk() const {
-    const long long left = u1 - u;
-    int n = KT - kt < kChunk ? KT - kt : kChunk;
-    return left < n ? static_cast<int>(left) : n;
-  }
-  __device__ void next() {
-    const int n = nk();
-    u += n;
-    kt += n;
-    if (kt == KT) kt = 0, ++rb;
-  }
-};
-
-__device__ __forceinline__ long long unit_start(long long c, long long U, long long G) {
-  return c * U / G;
+// Units are (256-row block, k-tile) pairs, u = rb * KT + kt; CTA c owns [start(c), start(c+1)).
+__device__ __forceinline__ int unit_start(int c, int U, int G) {
+  return static_cast<int>(static_cast<long long>(c) * U / G);
 }
 // CTA owning unit u: the largest c with unit_start(c) <= u (G <= U: every range non-empty).
-__device__ __forceinline__ long long unit_owner(long long u, long long U, long long G) {
-  return ((u + 1) * G - 1) / U;
+__device__ __forceinline__ int unit_owner(int u, int U, int G) {
+  return static_cast<int>((static_cast<long long>(u + 1) * G - 1) / U);
 }
+
+// Pipeline position shared by producer and consumers (CUTLASS convention: the producer
+// waits on `empty` with the opposite parity, so its first pass through the ring is free).
+struct Ring {
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ void advance() {
+    if (++stage == kStages) stage = 0, phase ^= 1u;
+  }
+};
 
 // One k-tile of the consumer loop for a warp's two row tiles: decode, gather the B
 // fragments of every batch block from the natural-layout activations, 2*J*NB MMAs.
+// Activation rows >= M are zero in shared memory, so the loads are unpredicated.
 template <int SCHEME, int NB>
 __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const uint4 (&wv)[2],
                                               const uint32_t (&sh)[2], float (&acc)[2][NB][4],
-                                              int g, int t, int M) {
+                                              int g, int t) {
   using T = Traits<SCHEME>;
   using LY = K2Layout<SCHEME, NB>;
   constexpr int J = T::kJ;
@@ -181,26 +172,19 @@ __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const u
   }
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    const int m = nb * 8 + g;
-    const uint8_t* xp = st + LY::kWBytes + m * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
+    const uint8_t* xp =
+        st + LY::kWBytes + (nb * 8 + g) * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
     uint32_t B[J][2];
     if constexpr (SCHEME == 4) {
-      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (m < M) {
-        const uint4 a = *reinterpret_cast<const uint4*>(xp);
-        const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
-        w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w;
-        w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
-      }
+      const uint4 a = *reinterpret_cast<const uint4*>(xp);
+      const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
       bfrag_s4(w, B);
     } else {
-      uint32_t w[6] = {0, 0, 0, 0, 0, 0};
-      if (m < M) {
-        const uint2 a = *reinterpret_cast<const uint2*>(xp);
-        const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
-        const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
-        w[0] = a.x, w[1] = a.y, w[2] = b.x, w[3] = b.y, w[4] = d.x, w[5] = d.y;
-      }
+      const uint2 a = *reinterpret_cast<const uint2*>(xp);
+      const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
+      const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
+      const uint32_t w[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
       bfrag_s7(w, B);
     }
 #pragma unroll
@@ -215,21 +199,22 @@ template <int SCHEME, int NB>
 __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(LinearParams p) {
   using T = Traits<SCHEME>;
   using LY = K2Layout<SCHEME, NB>;
-  constexpr int J = T::kJ;
   constexpr int TILE = T::kTileBytes;
+  constexpr int MS = 8 * NB;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff);
   uint64_t* empty = full + kStages;
-  int* flag = reinterpret_cast<int*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long U = static_cast<long long>(p.row_blocks) * p.k_tiles;
-  const long long G = gridDim.x;
-  const long long c = blockIdx.x;
-  const long long u0 = unit_start(c, U, G), u1 = unit_start(c + 1, U, G);
   const int KT = p.k_tiles;
+  const int U = p.row_blocks * KT;
+  const int G = gridDim.x;
+  const int c = blockIdx.x;
+  const int u0 = unit_start(c, U, G), u1 = unit_start(c + 1, U, G);
+  const int rb_first = u0 / KT, rb_last = (u1 - 1) / KT;
   unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+  pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -237,6 +222,12 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
+  }
+  // activation rows >= M are never written by the producer: zero them once
+  for (int s = 0; s < kStages; ++s) {
+    uint4* xz = reinterpret_cast<uint4*>(smem + s * LY::kStageBytes + LY::kWBytes + p.M * LY::kXRow);
+    const int n16 = (MS - p.M) * LY::kXRow / 16;
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) xz[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
 
@@ -249,39 +240,51 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
     const bool x_vec = ((p.cols & 7) == 0) && ((p.ldx & 7) == 0) &&
                        ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
     constexpr int kXUnits = kChunk * T::kTK * 2 / 16;  // 16-byte units per activation row
-    ChunkIter it(u0, u1, KT);
-    for (int i = 0; it.valid(); ++i, it.next()) {
-      const int s = i % kStages;
-      if (i >= kStages) mbar_wait(&empty[s], static_cast<uint32_t>((i / kStages) - 1) & 1u);
-      const int nk = it.nk();
-      uint8_t* st = smem + s * LY::kStageBytes;
-      const long long k0 = static_cast<long long>(it.kt) * T::kTK;
-      if (lane == 0) {
-        fence_proxy_async_smem();
-        const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
-        mbar_arrive_expect_tx(&full[s], wbytes);
-        bulk_g2s(st, p.w + (static_cast<long long>(it.rb) * KT + it.kt) * 16LL * TILE, wbytes,
-                 &full[s], pol);
-      }
-      const int units = p.M * kXUnits;
-      if (x_vec) {
-        for (int u = lane; u < units; u += 32) {
-          const int m = u / kXUnits, q = u - m * kXUnits;
-          const long long k = k0 + q * 8;
-          const long long left = p.cols - k;
-          const uint32_t nbytes = left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
-          const unsigned short* src = p.x + m * p.ldx + (nbytes ? k : 0);
-          cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16, src, nbytes);
+    const int units = p.M * kXUnits;
+    Ring ring;
+    bool waited = false;
+    for (int rb = rb_first; rb <= rb_last; ++rb) {
+      const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
+      const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
+      for (int kt = kt0; kt < kt1; kt += kChunk, ring.advance()) {
+        const int nk = min(kChunk, kt1 - kt);
+        mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+        uint8_t* st = smem + ring.stage * LY::kStageBytes;
+        uint64_t* fb = &full[ring.stage];
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
+          mbar_arrive_expect_tx(fb, wbytes);
+          bulk_g2s(st, p.w + (static_cast<long long>(rb) * KT + kt) * 16LL * TILE, wbytes, fb,
+                   pol);
         }
-        cp_async_mbar_arrive(&full[s]);
-      } else {  // unaligned activations: plain loads, then a regular arrival
-        for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
-          const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
-          unsigned short* xr = reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
-          xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e) : static_cast<unsigned short>(0);
+        const long long k0 = static_cast<long long>(kt) * T::kTK;
+        if (!waited) {  // weights are independent of the previous kernel; activations are not
+          pdl_wait();
+          waited = true;
         }
-        __threadfence_block();
-        mbar_arrive(&full[s]);
+        if (x_vec) {
+          for (int u = lane; u < units; u += 32) {
+            const int m = u / kXUnits, q = u - m * kXUnits;
+            const long long k = k0 + q * 8;
+            const long long left = p.cols - k;
+            const uint32_t nbytes =
+                left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
+            cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16,
+                        p.x + m * p.ldx + (nbytes ? k : 0), nbytes);
+          }
+          cp_async_mbar_arrive(fb);
+        } else {  // unaligned activations: plain loads, then a regular arrival
+          for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
+            const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
+            unsigned short* xr =
+                reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
+            xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e)
+                                      : static_cast<unsigned short>(0);
+          }
+          __threadfence_block();
+          mbar_arrive(fb);
+        }
       }
     }
     return;
@@ -289,22 +292,24 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
 
   // -------------------------------------------------------------- consumer warps
   const int g = lane >> 2, t = lane & 3;
-  float acc[2][NB][4];
-  auto zero_acc = [&] {
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[rr][nb][e] = 0.0f;
-  };
-  zero_acc();
-  int cur_rb = -1, seg_kt0 = 0, seg_kt1 = 0;
   constexpr int kCons = kConsumerWarps * 32;
+  float acc[2][NB][4];
 
-  auto finish_segment = [&](int rb) {
-    const int rib0 = 32 * warp;
-    if (seg_kt0 == 0 && seg_kt1 == KT) {  // this CTA covered the whole K range
+  // End of a row-block segment. Full K range covered by this CTA: scale and store y.
+  // Otherwise publish this warp's 32-row slice as an fp32 partial and take a ticket on the
+  // slice's counter (release, result not consumed until the end of the CTA's work); the
+  // last contributor of a slice reduces it after the main loop, summing the partials in
+  // CTA order (deterministic). No CTA-wide barrier sits on the streaming path.
+  // at most two partial segments per CTA (its first and its last row block)
+  int pend_rb0 = -1, pend_t0 = 0, pend_rb1 = -1, pend_t1 = 0;
+  const int rib0 = 32 * warp;
+  bool waited = false;
+  auto finish_segment = [&](int rb, bool full_k) {
+    if (!waited) {  // outputs / workspace may still be in use by the previous kernel
+      pdl_wait();
+      waited = true;
+    }
+    if (full_k) {
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
@@ -327,9 +332,7 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
       }
       return;
     }
-    constexpr int MS = 8 * NB;
-    const long long pid = c + rb;
-    float* part = p.partials + pid * MS * 256;
+    float* part = p.partials + (static_cast<long long>(c) + rb) * MS * 256;
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
@@ -341,104 +344,120 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
             const int m = nb * 8 + 2 * t + e;
             part[m * 256 + rib0 + rr * 16 + g + 8 * h] = acc[rr][nb][2 * h + e];
           }
-    named_bar_sync(1, kCons);  // all partial stores of this CTA happen-before thread 0's ticket
-    const long long c_first = unit_owner(static_cast<long long>(rb) * KT, U, G);
-    const long long c_last = unit_owner(static_cast<long long>(rb + 1) * KT - 1, U, G);
-    if (threadIdx.x == 0) {
-      const int ncontrib = static_cast<int>(c_last - c_first + 1);
-      const int old = atomic_add_acq_rel_gpu(&p.counters[rb], 1);
-      const int last = (old == ncontrib - 1);
-      if (last) store_relaxed_gpu(&p.counters[rb], 0);  // self-cleaning for the next launch
-      *flag = last;
+    __syncwarp();  // the warp's partial stores happen-before lane 0's release
+    int ticket = 0;
+    if (lane == 0) ticket = atomic_add_acq_rel_gpu(&p.counters[rb * kConsumerWarps + warp], 1);
+    if (pend_rb0 < 0) {
+      pend_rb0 = rb, pend_t0 = ticket;
+    } else {
+      pend_rb1 = rb, pend_t1 = ticket;
     }
-    named_bar_sync(1, kCons);
-    if (*flag) {
-      // Sum the contributors' partials in CTA order (deterministic). All loads of a batch
-      // are issued before any add so the L2 latency is paid once per batch, not per term.
-      const int ncon = static_cast<int>(c_last - c_first + 1);
-      const float4* base = reinterpret_cast<const float4*>(p.partials + (c_first + rb) * MS * 256);
-      constexpr int kB = 8;
-      for (int o = threadIdx.x; o < p.M * 64; o += kCons) {
-        const int m = o >> 6, q = o & 63;
-        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int c0 = 0; c0 < ncon; c0 += kB) {
-          float4 v[kB];
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            v[j] = (c0 + j < ncon) ? __ldcg(base + ((c0 + j) * MS + m) * 64 + q)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            if (c0 + j < ncon) {
-              sum.x += v[j].x, sum.y += v[j].y, sum.z += v[j].z, sum.w += v[j].w;
-            }
-          }
-        }
-        const float r4[4] = {sum.x, sum.y, sum.z, sum.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const long long n = static_cast<long long>(rb) * 256 + 4 * q + e;
-          if (n < p.rows) {
-            const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
-            p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(r4[e] * sc));
-          }
-        }
-      }
-    }
-    named_bar_sync(1, kCons);
   };
 
-  ChunkIter it(u0, u1, KT);
-  for (int i = 0; it.valid(); ++i, it.next()) {
-    const int s = i % kStages;
-    const int nk = it.nk();
-    if (it.rb != cur_rb) {
-      if (cur_rb >= 0) finish_segment(cur_rb);
-      zero_acc();
-      cur_rb = it.rb;
-      seg_kt0 = it.kt;
-    }
-    seg_kt1 = it.kt + nk;
-    mbar_wait(&full[s], static_cast<uint32_t>(i / kStages) & 1u);
-    if (trace && i == 0 && threadIdx.x == 0) trace[1] = globaltimer();
-    const uint8_t* st = smem + s * LY::kStageBytes;
-    const uint8_t* wt = st + (2 * warp) * TILE + lane * 16;  // stage: [kk][16 row tiles]
-    if (p.dry) {
-      // profiling mode: stream only
-    } else if (nk == kChunk) {
-      // common case: guard-free, fully unrolled so loads of later k-tiles overlap the
-      // decode/MMA of earlier ones
-      uint4 wv[kChunk][2];
-      uint32_t sh[kChunk][2];
+  // Deferred reduction of a 32-row slice whose partials are all published.
+  auto reduce_slice = [&](int rb) {
+    const int c_first = unit_owner(rb * KT, U, G);
+    const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - c_first + 1;
+    const float4* base = reinterpret_cast<const float4*>(
+        p.partials + (static_cast<long long>(c_first) + rb) * MS * 256 + rib0);
+    constexpr int kB = 8;
+    for (int o = lane; o < p.M * 8; o += 32) {  // (m, 4-row group) of this 32-row slice
+      const int m = o >> 3, q = o & 7;
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < ncon; c0 += kB) {
+        float4 v[kB];
 #pragma unroll
-      for (int kk = 0; kk < kChunk; ++kk)
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
-          wv[kk][rr] = *reinterpret_cast<const uint4*>(tp);
-          sh[kk][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+        for (int j = 0; j < kB; ++j) {
+          v[j] = (c0 + j < ncon) ? __ldcg(base + ((c0 + j) * MS + m) * 64 + q)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-      for (int kk = 0; kk < kChunk; ++kk) consume_ktile<SCHEME, NB>(st, kk, wv[kk], sh[kk], acc, g, t, p.M);
-    } else {
-      for (int kk = 0; kk < nk; ++kk) {
-        uint4 wv[2];
-        uint32_t sh[2];
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
-          wv[rr] = *reinterpret_cast<const uint4*>(tp);
-          sh[rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+        for (int j = 0; j < kB; ++j) {
+          if (c0 + j < ncon) sum.x += v[j].x, sum.y += v[j].y, sum.z += v[j].z, sum.w += v[j].w;
         }
-        consume_ktile<SCHEME, NB>(st, kk, wv, sh, acc, g, t, p.M);
+      }
+      const float r4[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long n = static_cast<long long>(rb) * 256 + rib0 + 4 * q + e;
+        if (n < p.rows) {
+          const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+          p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(r4[e] * sc));
+        }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+  };
+
+  Ring ring;
+  bool first = true;
+  const uint8_t* wlane = smem + (2 * warp) * TILE + lane * 16;  // + stage base; [kk][16 row tiles]
+  for (int rb = rb_first; rb <= rb_last; ++rb) {
+    const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
+    const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[rr][nb][e] = 0.0f;
+    for (int kt = kt0; kt < kt1; kt += kChunk, ring.advance()) {
+      const int nk = min(kChunk, kt1 - kt);
+      mbar_wait(&full[ring.stage], ring.phase);
+      if (trace && first && threadIdx.x == 0) trace[1] = globaltimer();
+      first = false;
+      const uint8_t* st = smem + ring.stage * LY::kStageBytes;
+      const uint8_t* wt = wlane + ring.stage * LY::kStageBytes;
+      if (p.dry) {
+        // profiling mode: stream only
+      } else if (nk == kChunk) {
+        // common case: guard-free and fully unrolled so the loads of later k-tiles overlap
+        // the decode/MMA of earlier ones
+        uint4 wv[kChunk][2];
+        uint32_t sh[kChunk][2];
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk)
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
+            wv[kk][rr] = *reinterpret_cast<const uint4*>(tp);
+            sh[kk][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+          }
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) consume_ktile<SCHEME, NB>(st, kk, wv[kk], sh[kk], acc, g, t);
+      } else {
+        for (int kk = 0; kk < nk; ++kk) {
+          uint4 wv[2];
+          uint32_t sh[2];
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
+            wv[rr] = *reinterpret_cast<const uint4*>(tp);
+            sh[rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+          }
+          consume_ktile<SCHEME, NB>(st, kk, wv, sh, acc, g, t);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ring.stage]);
+    }
+    if (trace && rb == rb_last && threadIdx.x == 0) trace[2] = globaltimer();
+    finish_segment(rb, kt0 == 0 && kt1 == KT);
   }
-  if (trace && threadIdx.x == 0) trace[2] = globaltimer();
-  if (cur_rb >= 0) finish_segment(cur_rb);
+  // Slices this warp completed last: reduce them (the acquire in the ticket makes the other
+  // contributors' partials visible to lane 0; __syncwarp extends that to the warp).
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int rb = i == 0 ? pend_rb0 : pend_rb1;
+    if (rb < 0) continue;
+    const int ticket = i == 0 ? pend_t0 : pend_t1;
+    const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - unit_owner(rb * KT, U, G) + 1;
+    const int last = __shfl_sync(0xffffffffu, ticket == ncon - 1 ? 1 : 0, 0);
+    __syncwarp();
+    if (last) {
+      if (lane == 0) store_relaxed_gpu(&p.counters[rb * kConsumerWarps + warp], 0);
+      reduce_slice(rb);
+    }
+  }
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
 }
 
@@ -470,9 +489,19 @@ static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dev::amsq_linear_kernel<SCHEME, NB><<<grid, dev::kK2Threads, SM::kBytes, s>>>(p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(dev::kK2Threads);
+  cfg.dynamicSmemBytes = SM::kBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_kernel<SCHEME, NB>, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 int linear_max_batch_per_launch() { return 16; }

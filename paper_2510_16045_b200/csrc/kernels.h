@@ -29,7 +29,7 @@ struct LinearParams {
   const unsigned short* x;  // [M][ldx] fp16 (logical cols)
   unsigned short* y;        // [M][ldy] fp16
   float* partials;          // [(grid + row_blocks)][16][256] fp32
-  int* counters;            // [row_blocks], zero between launches
+  int* counters;            // [row_blocks][8 warp slices], zero between launches
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
   int row_blocks, k_tiles;
