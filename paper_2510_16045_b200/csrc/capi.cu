@@ -132,8 +132,7 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   amsqb::repack_to_device(h->L, payload + row0 * wpr, tiles.data(), 0);
   std::vector<unsigned short> sc(h->L.row_tiles * 16, 0);
   std::memcpy(sc.data(), scales + row0, nrows * sizeof(uint16_t));
-  const size_t grid = static_cast<size_t>(amsqb::linear_grid(
-      static_cast<long long>(h->L.row_blocks() * h->L.k_tiles)));
+  const size_t grid = static_cast<size_t>(amsqb::kMaxGridCTAs);
   const size_t partial_floats = (grid + h->L.row_blocks()) * 16 * 256;
   cudaStream_t st = as_stream(stream);
   ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");

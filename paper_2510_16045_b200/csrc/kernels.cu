@@ -108,12 +108,19 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
 // evenly over the grid (stream-K); a row block cut between CTAs is finished by the
 // last contributor, which sums the fp32 partials in CTA order (deterministic).
 // =====================================================================================
-constexpr int kConsumerWarps = 8;
-constexpr int kK2Threads = (kConsumerWarps + 1) * 32;
-constexpr int kChunk = 3;    // k-tiles per stage: 24-26 KB bulk copies (>= 16 KB, tools/tma_probe.cu)
-constexpr int kStages = 3;   // ring depth (two CTAs per SM share the 228 KB)
-constexpr int kCtasPerSM = 2;
+constexpr int kGroupWarps = 8;                   // a consumer group covers a 256-row block
+constexpr int kGroups = 2;                       // groups split every stage's k-tiles
+constexpr int kConsumerWarps = kGroups * kGroupWarps;
+constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
+constexpr int kChunk = 4;    // k-tiles per stage: 32-35 KB bulk copies (>= 16 KB, tools/tma_probe.cu)
+constexpr int kGroupK = kChunk / kGroups;        // k-tiles of a stage each group consumes
+constexpr int kMaxStages = 5;  // ring depth (fewer when the stage is large, see K2Layout);
+                               // a <= 113 KB variant that lets PDL successors co-reside was
+                               // measured slower (too few bytes in flight)
 
+// One CTA per SM: co-resident CTAs were measured to starve each other at the warp arbiter
+// (the lower-priority CTA finishes ~40% later), so each SM runs a single CTA whose two
+// consumer groups each take half of every stage's k-tiles (balanced at segment ends).
 template <int SCHEME, int NB>
 struct K2Layout {
   using T = Traits<SCHEME>;
@@ -125,10 +132,14 @@ struct K2Layout {
   static constexpr int kXTarget = SCHEME == 7 ? 96 : 16;
   static constexpr int kXRow = kXRaw + ((kXTarget - kXRaw % 128) + 128) % 128;
   static constexpr int kStageBytes = kWBytes + kMS * kXRow;
-  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kScratchBytes = kGroupWarps * 32 * 2 * NB * 4 * 4;
+  static constexpr int kFit = (227 * 1024 - kScratchBytes - 1024) / kStageBytes;
+  static constexpr int kStages = kFit < kMaxStages ? kFit : kMaxStages;
+  static constexpr int kScratchOff = kStages * kStageBytes;  // group-1 accumulators
+  static constexpr int kBarOff = kScratchOff + kScratchBytes;
   static constexpr int kBytes = kBarOff + 2 * kStages * 8 + 16;
   static_assert(kWBytes % 16 == 0 && kXRow % 16 == 0 && kStageBytes % 16 == 0, "alignment");
-  static_assert(kBytes <= 113 * 1024, "two CTAs per SM must fit in shared memory");
+  static_assert(kBytes <= 227 * 1024, "shared memory budget");
 };
 
 // Units are (256-row block, k-tile) pairs, u = rb * KT + kt; CTA c owns [start(c), start(c+1)).
@@ -140,20 +151,10 @@ __device__ __forceinline__ int unit_owner(int u, int U, int G) {
   return static_cast<int>((static_cast<long long>(u + 1) * G - 1) / U);
 }
 
-// Pipeline position shared by producer and consumers (CUTLASS convention: the producer
-// waits on `empty` with the opposite parity, so its first pass through the ring is free).
-struct Ring {
-  int stage = 0;
-  uint32_t phase = 0;
-  __device__ void advance() {
-    if (++stage == kStages) stage = 0, phase ^= 1u;
-  }
-};
-
 // One k-tile of the consumer loop for a warp's two row tiles: decode, gather the B
 // fragments of every batch block from the natural-layout activations, 2*J*NB MMAs.
 // Activation rows >= M are zero in shared memory, so the loads are unpredicated.
-template <int SCHEME, int NB>
+template <int SCHEME, int NB, int MODE = 0>  // MODE (profiling): 1 = no MMA, 2 = no decode
 __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const uint4 (&wv)[2],
                                               const uint32_t (&sh)[2], float (&acc)[2][NB][4],
                                               int g, int t) {
@@ -164,7 +165,12 @@ __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const u
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const uint32_t R[4] = {wv[rr].x, wv[rr].y, wv[rr].z, wv[rr].w};
-    if constexpr (SCHEME == 4) {
+    if constexpr (MODE == 2) {
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) A[rr][j][q] = R[(j + q) & 3] & 0x3F003F00u;
+    } else if constexpr (SCHEME == 4) {
       decode_s4(R, sh[rr], A[rr]);
     } else {
       decode_s7(R, A[rr]);
@@ -189,21 +195,28 @@ __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const u
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      mma16816(acc[0][nb], A[0][j], B[j][0], B[j][1]);
-      mma16816(acc[1][nb], A[1][j], B[j][0], B[j][1]);
+      if constexpr (MODE == 1) {  // keep the decode live without the tensor pipe
+        acc[0][nb][j & 3] += __uint_as_float((A[0][j][0] ^ A[0][j][1] ^ A[0][j][2] ^ A[0][j][3] ^ B[j][0]) & 0x3F0F0F0Fu);
+        acc[1][nb][j & 3] += __uint_as_float((A[1][j][0] ^ A[1][j][1] ^ A[1][j][2] ^ A[1][j][3] ^ B[j][1]) & 0x3F0F0F0Fu);
+      } else {
+        mma16816(acc[0][nb], A[0][j], B[j][0], B[j][1]);
+        mma16816(acc[1][nb], A[1][j], B[j][0], B[j][1]);
+      }
     }
   }
 }
 
-template <int SCHEME, int NB>
-__global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(LinearParams p) {
+template <int SCHEME, int NB, int MODE>
+__global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams p) {
   using T = Traits<SCHEME>;
   using LY = K2Layout<SCHEME, NB>;
   constexpr int TILE = T::kTileBytes;
   constexpr int MS = 8 * NB;
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kStages = LY::kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff);
   uint64_t* empty = full + kStages;
+  float* scratch = reinterpret_cast<float*>(smem + LY::kScratchOff);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = p.k_tiles;
@@ -241,16 +254,17 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
                        ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
     constexpr int kXUnits = kChunk * T::kTK * 2 / 16;  // 16-byte units per activation row
     const int units = p.M * kXUnits;
-    Ring ring;
+    int stage = 0;
+    uint32_t phase = 0;
     bool waited = false;
     for (int rb = rb_first; rb <= rb_last; ++rb) {
       const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
       const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
-      for (int kt = kt0; kt < kt1; kt += kChunk, ring.advance()) {
+      for (int kt = kt0; kt < kt1; kt += kChunk) {
         const int nk = min(kChunk, kt1 - kt);
-        mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
-        uint8_t* st = smem + ring.stage * LY::kStageBytes;
-        uint64_t* fb = &full[ring.stage];
+        mbar_wait(&empty[stage], phase ^ 1u);
+        uint8_t* st = smem + stage * LY::kStageBytes;
+        uint64_t* fb = &full[stage];
         if (lane == 0) {
           fence_proxy_async_smem();
           const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
@@ -285,98 +299,136 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
           __threadfence_block();
           mbar_arrive(fb);
         }
+        if (++stage == kStages) stage = 0, phase ^= 1u;
       }
     }
     return;
   }
 
   // -------------------------------------------------------------- consumer warps
+  // group gr = warp / 8 consumes the stages of parity gr (chunks 2j + gr of the CTA's
+  // sequence); warp wg = warp % 8 owns row tiles 2wg, 2wg+1 of the 256-row block.
+  const int gr = warp / kGroupWarps, wg = warp % kGroupWarps;
   const int g = lane >> 2, t = lane & 3;
   constexpr int kCons = kConsumerWarps * 32;
   float acc[2][NB][4];
-
-  // End of a row-block segment. Full K range covered by this CTA: scale and store y.
-  // Otherwise publish this warp's 32-row slice as an fp32 partial and take a ticket on the
-  // slice's counter (release, result not consumed until the end of the CTA's work); the
-  // last contributor of a slice reduces it after the main loop, summing the partials in
-  // CTA order (deterministic). No CTA-wide barrier sits on the streaming path.
-  // at most two partial segments per CTA (its first and its last row block)
-  int pend_rb0 = -1, pend_t0 = 0, pend_rb1 = -1, pend_t1 = 0;
-  const int rib0 = 32 * warp;
   bool waited = false;
+
+  // End of a row-block segment: group 1 hands its accumulators to group 0 through shared
+  // memory (sum order g0 + g1: deterministic). Group 0 then either stores y (the CTA
+  // covered the whole K range) or publishes its 32-row slice as an fp32 partial and takes a
+  // ticket on the slice's counter (release; result consumed after the main loop, when the
+  // last contributor of a slice reduces it in CTA order).
+  int pend_rb0 = -1, pend_t0 = 0, pend_rb1 = -1, pend_t1 = 0;
+  const int rib0 = 32 * wg;
+  float* my_scratch = scratch + (wg * 32 + lane) * (2 * NB * 4);
   auto finish_segment = [&](int rb, bool full_k) {
     if (!waited) {  // outputs / workspace may still be in use by the previous kernel
       pdl_wait();
       waited = true;
     }
-    if (full_k) {
+    if (gr == 1) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
+      for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const long long n = static_cast<long long>(rb) * 256 + rib0 + rr * 16 + g + 8 * h;
-          if (n >= p.rows) continue;
-          const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+        for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) {
+          for (int e = 0; e < 4; ++e) my_scratch[(rr * NB + nb) * 4 + e] = acc[rr][nb][e];
+    }
+    named_bar_sync(1, kCons);
+    if (gr == 0) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int m = nb * 8 + 2 * t + e;
-              if (m < p.M) {
-                p.y[static_cast<long long>(m) * p.ldy + n] =
-                    __half_as_ushort(__float2half_rn(acc[rr][nb][2 * h + e] * sc));
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[rr][nb][e] += my_scratch[(rr * NB + nb) * 4 + e];
+      if (full_k) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const long long n = static_cast<long long>(rb) * 256 + rib0 + rr * 16 + g + 8 * h;
+            if (n >= p.rows) continue;
+            const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int m = nb * 8 + 2 * t + e;
+                if (m < p.M) {
+                  p.y[static_cast<long long>(m) * p.ldy + n] =
+                      __half_as_ushort(__float2half_rn(acc[rr][nb][2 * h + e] * sc));
+                }
               }
             }
           }
         }
+      } else {
+        float* part = p.partials + (static_cast<long long>(c) + rb) * MS * 256;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int m = nb * 8 + 2 * t + e;
+                part[m * 256 + rib0 + rr * 16 + g + 8 * h] = acc[rr][nb][2 * h + e];
+              }
+        __syncwarp();  // the warp's partial stores happen-before lane 0's release
+        int ticket = 0;
+        if (lane == 0) ticket = atomic_add_acq_rel_gpu(&p.counters[rb * kGroupWarps + wg], 1);
+        if (pend_rb0 < 0) {
+          pend_rb0 = rb, pend_t0 = ticket;
+        } else {
+          pend_rb1 = rb, pend_t1 = ticket;
+        }
       }
-      return;
     }
-    float* part = p.partials + (static_cast<long long>(c) + rb) * MS * 256;
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int m = nb * 8 + 2 * t + e;
-            part[m * 256 + rib0 + rr * 16 + g + 8 * h] = acc[rr][nb][2 * h + e];
-          }
-    __syncwarp();  // the warp's partial stores happen-before lane 0's release
-    int ticket = 0;
-    if (lane == 0) ticket = atomic_add_acq_rel_gpu(&p.counters[rb * kConsumerWarps + warp], 1);
-    if (pend_rb0 < 0) {
-      pend_rb0 = rb, pend_t0 = ticket;
-    } else {
-      pend_rb1 = rb, pend_t1 = ticket;
-    }
+    named_bar_sync(1, kCons);  // scratch free for the next segment
   };
 
-  // Deferred reduction of a 32-row slice whose partials are all published.
+  // Deferred reduction of a 32-row slice whose partials are all published: the slice is
+  // M x 8 float4 outputs, each the CTA-ordered sum of ncon partials. Every lane issues the
+  // loads of all its (output, contributor) pairs before adding, four contributors at a time.
   auto reduce_slice = [&](int rb) {
     const int c_first = unit_owner(rb * KT, U, G);
     const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - c_first + 1;
     const float4* base = reinterpret_cast<const float4*>(
         p.partials + (static_cast<long long>(c_first) + rb) * MS * 256 + rib0);
-    constexpr int kB = 8;
-    for (int o = lane; o < p.M * 8; o += 32) {  // (m, 4-row group) of this 32-row slice
+    const int nout = p.M * 8;  // outputs of the slice (<= 128): lane owns o = lane + 32 i
+    float4 sum[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sum[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < ncon; c0 += 4) {  // 16 independent loads in flight per lane
+      float4 v[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int o = lane + 32 * i;
+          v[i][j] = (o < nout && c0 + j < ncon)
+                        ? __ldcg(base + ((c0 + j) * MS + (o >> 3)) * 64 + (o & 7))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c0 + j < ncon) {  // contributor order c0, c0+1, ... : deterministic
+            sum[i].x += v[i][j].x, sum[i].y += v[i][j].y, sum[i].z += v[i][j].z,
+                sum[i].w += v[i][j].w;
+          }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int o = lane + 32 * i;
+      if (o >= nout) continue;
       const int m = o >> 3, q = o & 7;
-      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = 0; c0 < ncon; c0 += kB) {
-        float4 v[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          v[j] = (c0 + j < ncon) ? __ldcg(base + ((c0 + j) * MS + m) * 64 + q)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          if (c0 + j < ncon) sum.x += v[j].x, sum.y += v[j].y, sum.z += v[j].z, sum.w += v[j].w;
-        }
-      }
-      const float r4[4] = {sum.x, sum.y, sum.z, sum.w};
+      const float r4[4] = {sum[i].x, sum[i].y, sum[i].z, sum[i].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const long long n = static_cast<long long>(rb) * 256 + rib0 + 4 * q + e;
@@ -388,9 +440,11 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
     }
   };
 
-  Ring ring;
+  int stage = 0;
+  uint32_t phase = 0;
   bool first = true;
-  const uint8_t* wlane = smem + (2 * warp) * TILE + lane * 16;  // + stage base; [kk][16 row tiles]
+  const uint8_t* wlane = smem + (2 * wg) * TILE + lane * 16;  // + stage base; [kk][16 row tiles]
+  const int kkb = gr * kGroupK;  // this group's k-tiles of each stage: kkb .. kkb + kGroupK - 1
   for (int rb = rb_first; rb <= rb_last; ++rb) {
     const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
     const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
@@ -400,32 +454,33 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
       for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[rr][nb][e] = 0.0f;
-    for (int kt = kt0; kt < kt1; kt += kChunk, ring.advance()) {
+    for (int kt = kt0; kt < kt1; kt += kChunk) {
       const int nk = min(kChunk, kt1 - kt);
-      mbar_wait(&full[ring.stage], ring.phase);
+      mbar_wait(&full[stage], phase);
       if (trace && first && threadIdx.x == 0) trace[1] = globaltimer();
       first = false;
-      const uint8_t* st = smem + ring.stage * LY::kStageBytes;
-      const uint8_t* wt = wlane + ring.stage * LY::kStageBytes;
-      if (p.dry) {
+      const uint8_t* st = smem + stage * LY::kStageBytes;
+      const uint8_t* wt = wlane + stage * LY::kStageBytes;
+      if (p.dry == 1) {
         // profiling mode: stream only
       } else if (nk == kChunk) {
-        // common case: guard-free and fully unrolled so the loads of later k-tiles overlap
-        // the decode/MMA of earlier ones
-        uint4 wv[kChunk][2];
-        uint32_t sh[kChunk][2];
+        // common case: guard-free and fully unrolled so the loads of the second k-tile
+        // overlap the decode/MMA of the first
+        uint4 wv[kGroupK][2];
+        uint32_t sh[kGroupK][2];
 #pragma unroll
-        for (int kk = 0; kk < kChunk; ++kk)
+        for (int i = 0; i < kGroupK; ++i)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
-            const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
-            wv[kk][rr] = *reinterpret_cast<const uint4*>(tp);
-            sh[kk][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+            const uint8_t* tp = wt + ((kkb + i) * 16 + rr) * TILE;
+            wv[i][rr] = *reinterpret_cast<const uint4*>(tp);
+            sh[i][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
           }
 #pragma unroll
-        for (int kk = 0; kk < kChunk; ++kk) consume_ktile<SCHEME, NB>(st, kk, wv[kk], sh[kk], acc, g, t);
+        for (int i = 0; i < kGroupK; ++i)
+          consume_ktile<SCHEME, NB, MODE>(st, kkb + i, wv[i], sh[i], acc, g, t);
       } else {
-        for (int kk = 0; kk < nk; ++kk) {
+        for (int kk = kkb; kk < min(nk, kkb + kGroupK); ++kk) {
           uint4 wv[2];
           uint32_t sh[2];
 #pragma unroll
@@ -434,28 +489,31 @@ __global__ void __launch_bounds__(kK2Threads, kCtasPerSM) amsq_linear_kernel(Lin
             wv[rr] = *reinterpret_cast<const uint4*>(tp);
             sh[rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
           }
-          consume_ktile<SCHEME, NB>(st, kk, wv, sh, acc, g, t);
+          consume_ktile<SCHEME, NB, MODE>(st, kk, wv, sh, acc, g, t);
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[ring.stage]);
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kStages) stage = 0, phase ^= 1u;
     }
     if (trace && rb == rb_last && threadIdx.x == 0) trace[2] = globaltimer();
     finish_segment(rb, kt0 == 0 && kt1 == KT);
   }
   // Slices this warp completed last: reduce them (the acquire in the ticket makes the other
   // contributors' partials visible to lane 0; __syncwarp extends that to the warp).
+  if (gr == 0) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int rb = i == 0 ? pend_rb0 : pend_rb1;
-    if (rb < 0) continue;
-    const int ticket = i == 0 ? pend_t0 : pend_t1;
-    const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - unit_owner(rb * KT, U, G) + 1;
-    const int last = __shfl_sync(0xffffffffu, ticket == ncon - 1 ? 1 : 0, 0);
-    __syncwarp();
-    if (last) {
-      if (lane == 0) store_relaxed_gpu(&p.counters[rb * kConsumerWarps + warp], 0);
-      reduce_slice(rb);
+    for (int i = 0; i < 2; ++i) {
+      const int rb = i == 0 ? pend_rb0 : pend_rb1;
+      if (rb < 0) continue;
+      const int ticket = i == 0 ? pend_t0 : pend_t1;
+      const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - unit_owner(rb * KT, U, G) + 1;
+      const int last = __shfl_sync(0xffffffffu, ticket == ncon - 1 ? 1 : 0, 0);
+      __syncwarp();
+      if (last) {
+        if (lane == 0) store_relaxed_gpu(&p.counters[rb * kGroupWarps + wg], 0);
+        reduce_slice(rb);
+      }
     }
   }
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
@@ -479,12 +537,12 @@ cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int SCHEME, int NB>
-static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t s) {
+template <int SCHEME, int NB, int MODE>
+static cudaError_t launch_linear_m(const LinearParams& p, int grid, cudaStream_t s) {
   using SM = dev::K2Layout<SCHEME, NB>;
   static bool configured = false;  // per template instance; attribute is per-function
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB>,
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -499,18 +557,25 @@ static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_kernel<SCHEME, NB>, p);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_kernel<SCHEME, NB, MODE>, p);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+template <int SCHEME, int NB>
+static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t s) {
+  if (p.dry == 2) return launch_linear_m<SCHEME, NB, 1>(p, grid, s);  // profiling: no MMA
+  if (p.dry == 3) return launch_linear_m<SCHEME, NB, 2>(p, grid, s);  // profiling: no decode
+  return launch_linear_m<SCHEME, NB, 0>(p, grid, s);
+}
+
 int linear_max_batch_per_launch() { return 16; }
 
-long long linear_grid(long long units) { return units < kGridCTAs ? units : kGridCTAs; }
+long long linear_grid(long long units, int /*M*/) { return units < kSMs ? units : kSMs; }
 
-cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
+cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {  // NOLINT
   const long long units = static_cast<long long>(p.row_blocks) * p.k_tiles;
-  const int grid = static_cast<int>(linear_grid(units));
+  const int grid = static_cast<int>(linear_grid(units, p.M));
   if (grid <= 0) return cudaSuccess;
   if (p.scheme_id == 4) {
     return p.M <= 8 ? launch_linear_t<4, 1>(p, grid, s) : launch_linear_t<4, 2>(p, grid, s);

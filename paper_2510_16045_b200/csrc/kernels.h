@@ -7,9 +7,11 @@
 
 namespace amsqb {
 
-// Fixed persistent grid of the stream-K linear: the split-K partition (and therefore the
-// fp32 reduction order) depends only on the shape, never on the device it runs on.
-constexpr long long kGridCTAs = 2 * 148;  // two CTAs per SM on the 148-SM B200
+// Fixed persistent grid of the stream-K linear (one CTA per SM of the 148-SM B200): the
+// split-K partition, and therefore the fp32 reduction order, depends only on the shape,
+// never on the device it runs on.
+constexpr long long kSMs = 148;
+constexpr long long kMaxGridCTAs = kSMs;
 
 struct RestoreParams {
   int scheme_id;
@@ -29,7 +31,7 @@ struct LinearParams {
   const unsigned short* x;  // [M][ldx] fp16 (logical cols)
   unsigned short* y;        // [M][ldy] fp16
   float* partials;          // [(grid + row_blocks)][16][256] fp32
-  int* counters;            // [row_blocks][8 warp slices], zero between launches
+  int* counters;            // [row_blocks][8 32-row slices], zero between launches
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
   int row_blocks, k_tiles;
@@ -41,7 +43,7 @@ cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
 cudaError_t launch_unshard(const unsigned short* in, int P, int batch, int n, unsigned short* out,
                            cudaStream_t s);
-long long linear_grid(long long units);
+long long linear_grid(long long units, int M);
 int linear_max_batch_per_launch();
 uint64_t kernel_launch_count();
 
