@@ -25,6 +25,7 @@ struct amsq_weight_s {
   unsigned short* d_scales = nullptr;
   float* d_partials = nullptr;
   int* d_counters = nullptr;
+  uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 16 batch rows)
 };
 
 namespace {
@@ -139,6 +140,7 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
   ck(cudaMalloc(&h->d_partials, partial_floats * sizeof(float)), "cudaMalloc(partials)");
   ck(cudaMalloc(&h->d_counters, h->L.row_blocks() * 8 * sizeof(int)), "cudaMalloc(counters)");
+  ck(cudaMalloc(&h->d_xperm, h->L.k_tiles * 4 * 16 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
   ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
   ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
   ck(cudaMemsetAsync(h->d_counters, 0, h->L.row_blocks() * 8 * sizeof(int), st), "memset counters");
@@ -153,6 +155,7 @@ void free_impl(amsq_weight_t h) {
   cudaFree(h->d_scales);
   cudaFree(h->d_partials);
   cudaFree(h->d_counters);
+  cudaFree(h->d_xperm);
   delete h;
 }
 
@@ -169,6 +172,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.scales = h->d_scales;
   p.partials = h->d_partials;
   p.counters = h->d_counters;
+  p.xperm = h->d_xperm;
   p.rows = static_cast<long long>(h->L.rows);
   p.cols = static_cast<long long>(h->L.cols);
   p.ldx = p.cols;

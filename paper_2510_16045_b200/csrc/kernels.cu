@@ -96,6 +96,46 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
 }
 
 // =====================================================================================
+// Activation prep for K2: x[M][cols] (fp16, row stride ldx) -> B-fragment units
+// xp[kt][j][m][t] (8 bytes: the two fp16 pairs lane t of an m16n8k16 MMA j reads for batch
+// row m), zero for m >= M and k >= cols. One thread per (k-tile, row, lane-column) item.
+// =====================================================================================
+template <int SCHEME>
+__global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* __restrict__ x,
+                                                         long long ldx, long long cols, int M,
+                                                         int MS, int KT, uint2* __restrict__ xp) {
+  using T = Traits<SCHEME>;
+  constexpr int J = T::kJ, LK = T::kLaneK, LW = LK / 2;
+  pdl_launch_dependents();
+  pdl_wait();  // x is produced by the previous kernel in the stream
+  const int items = KT * MS * 4;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < items; u += gridDim.x * blockDim.x) {
+    const int kt = u / (MS * 4), r = u - kt * MS * 4, m = r >> 2, t = r & 3;
+    const long long k = static_cast<long long>(kt) * T::kTK + t * LK;
+    uint32_t w[LW];
+#pragma unroll
+    for (int i = 0; i < LW; ++i) {
+      unsigned lo = 0, hi = 0;
+      if (m < M) {
+        if (k + 2 * i < cols) lo = __ldg(x + m * ldx + k + 2 * i);
+        if (k + 2 * i + 1 < cols) hi = __ldg(x + m * ldx + k + 2 * i + 1);
+      }
+      w[i] = lo | hi << 16;
+    }
+    uint32_t B[J][2];
+    if constexpr (SCHEME == 4) {
+      bfrag_s4(w, B);
+    } else {
+      bfrag_s7(w, B);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      xp[((static_cast<long long>(kt) * J + j) * MS + m) * 4 + t] = make_uint2(B[j][0], B[j][1]);
+    }
+  }
+}
+
+// =====================================================================================
 // K2: fused restore + linear, M <= 8*NB (NB = 1 or 2).
 //
 // Warp-specialised persistent CTA (one per SM): warp 8 is the producer -- its lane 0
@@ -126,19 +166,24 @@ struct K2Layout {
   using T = Traits<SCHEME>;
   static constexpr int kMS = 8 * NB;
   static constexpr int kWBytes = 16 * kChunk * T::kTileBytes;
-  // activation row stride padded so the lanes' LDS hit distinct banks:
-  // stride = 96 (mod 128) bytes for the 24-byte FP5.33 lane runs, 16 (mod 128) for FP4.25
+  // Activations of a stage. M <= 8 (NB = 1): natural row-major rows loaded by LDGSTS, the
+  // row stride padded so the lanes' LDS hit distinct banks (96 (mod 128) bytes for the
+  // 24-byte FP5.33 lane runs, 16 (mod 128) for FP4.25) and B fragments gathered with PRMT.
+  // M <= 16 (NB = 2): B-fragment-order units ((kk * J + j) * MS + m) * 4 + t written by
+  // amsq_xprep_kernel and bulk-copied, one conflict-free LDS.64 per MMA.
+  static constexpr bool kXPrep = NB == 2;
   static constexpr int kXRaw = kChunk * T::kTK * 2;
   static constexpr int kXTarget = SCHEME == 7 ? 96 : 16;
   static constexpr int kXRow = kXRaw + ((kXTarget - kXRaw % 128) + 128) % 128;
-  static constexpr int kStageBytes = kWBytes + kMS * kXRow;
+  static constexpr int kXBytes = kXPrep ? kChunk * T::kJ * kMS * 4 * 8 : kMS * kXRow;
+  static constexpr int kStageBytes = kWBytes + kXBytes;
   static constexpr int kScratchBytes = kGroupWarps * 32 * 2 * NB * 4 * 4;
   static constexpr int kFit = (227 * 1024 - kScratchBytes - 1024) / kStageBytes;
   static constexpr int kStages = kFit < kMaxStages ? kFit : kMaxStages;
   static constexpr int kScratchOff = kStages * kStageBytes;  // group-1 accumulators
   static constexpr int kBarOff = kScratchOff + kScratchBytes;
   static constexpr int kBytes = kBarOff + 2 * kStages * 8 + 16;
-  static_assert(kWBytes % 16 == 0 && kXRow % 16 == 0 && kStageBytes % 16 == 0, "alignment");
+  static_assert(kWBytes % 16 == 0 && kStageBytes % 16 == 0, "alignment");
   static_assert(kBytes <= 227 * 1024, "shared memory budget");
 };
 
@@ -178,20 +223,31 @@ __device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const u
   }
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    const uint8_t* xp =
-        st + LY::kWBytes + (nb * 8 + g) * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
     uint32_t B[J][2];
-    if constexpr (SCHEME == 4) {
-      const uint4 a = *reinterpret_cast<const uint4*>(xp);
-      const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
-      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      bfrag_s4(w, B);
+    if constexpr (LY::kXPrep) {
+      const uint2* xs = reinterpret_cast<const uint2*>(st + LY::kWBytes) +
+                        ((kk * J) * LY::kMS + nb * 8 + g) * 4 + t;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const uint2 b = xs[j * LY::kMS * 4];
+        B[j][0] = b.x;
+        B[j][1] = b.y;
+      }
     } else {
-      const uint2 a = *reinterpret_cast<const uint2*>(xp);
-      const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
-      const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
-      const uint32_t w[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
-      bfrag_s7(w, B);
+      const uint8_t* xp =
+          st + LY::kWBytes + (nb * 8 + g) * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
+      if constexpr (SCHEME == 4) {
+        const uint4 a = *reinterpret_cast<const uint4*>(xp);
+        const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        bfrag_s4(w, B);
+      } else {
+        const uint2 a = *reinterpret_cast<const uint2*>(xp);
+        const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
+        const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
+        const uint32_t w[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
+        bfrag_s7(w, B);
+      }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -231,25 +287,31 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1 + 32);  // expect_tx arrival + one per producer lane
+      // the producer's arrive.expect_tx, plus one LDGSTS arrival per producer lane when the
+      // activations are loaded in natural layout
+      mbar_init(&full[s], LY::kXPrep ? 1 : 1 + 32);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
-  // activation rows >= M are never written by the producer: zero them once
-  for (int s = 0; s < kStages; ++s) {
-    uint4* xz = reinterpret_cast<uint4*>(smem + s * LY::kStageBytes + LY::kWBytes + p.M * LY::kXRow);
-    const int n16 = (MS - p.M) * LY::kXRow / 16;
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) xz[i] = make_uint4(0, 0, 0, 0);
+  // natural-layout activation rows >= M are never written by the producer: zero them once
+  if constexpr (!LY::kXPrep) {
+    for (int s = 0; s < kStages; ++s) {
+      uint4* xz = reinterpret_cast<uint4*>(smem + s * LY::kStageBytes + LY::kWBytes + p.M * LY::kXRow);
+      const int n16 = (MS - p.M) * LY::kXRow / 16;
+      for (int i = threadIdx.x; i < n16; i += blockDim.x) xz[i] = make_uint4(0, 0, 0, 0);
+    }
   }
   __syncthreads();
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer warp
-    // lane 0: one bulk copy of the stage's 16*nk weight tiles (contiguous in the
-    // [row_block][k_tile][row_tile] layout); all lanes: the activation rows with 16-byte
-    // LDGSTS (zero-filled past `cols`), each lane arriving once on the full barrier.
+    // lane 0, per stage: one bulk copy of the 16*nk weight tiles (contiguous in the
+    // [row_block][k_tile][row_tile] layout). Activations: NB = 2 -> one more bulk copy of the
+    // prepped B-fragment units; NB = 1 -> all lanes LDGSTS the natural rows (zero-filled
+    // past `cols`), each lane arriving once on the full barrier when its copies land.
     const uint64_t pol = policy_evict_first();
+    constexpr uint32_t kXTileBytes = T::kJ * MS * 4 * 8;
     const bool x_vec = ((p.cols & 7) == 0) && ((p.ldx & 7) == 0) &&
                        ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
     constexpr int kXUnits = kChunk * T::kTK * 2 / 16;  // 16-byte units per activation row
@@ -265,39 +327,52 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
         mbar_wait(&empty[stage], phase ^ 1u);
         uint8_t* st = smem + stage * LY::kStageBytes;
         uint64_t* fb = &full[stage];
+        const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
+        const uint32_t xbytes =
+            (LY::kXPrep && p.dry != 4) ? static_cast<uint32_t>(nk) * kXTileBytes : 0u;
         if (lane == 0) {
           fence_proxy_async_smem();
-          const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
-          mbar_arrive_expect_tx(fb, wbytes);
+          mbar_arrive_expect_tx(fb, wbytes + xbytes);
           bulk_g2s(st, p.w + (static_cast<long long>(rb) * KT + kt) * 16LL * TILE, wbytes, fb,
                    pol);
         }
-        const long long k0 = static_cast<long long>(kt) * T::kTK;
-        if (!waited) {  // weights are independent of the previous kernel; activations are not
+        if (!waited) {  // weights are independent of the previous kernel; activations not
           pdl_wait();
           waited = true;
         }
-        if (x_vec) {
-          for (int u = lane; u < units; u += 32) {
-            const int m = u / kXUnits, q = u - m * kXUnits;
-            const long long k = k0 + q * 8;
-            const long long left = p.cols - k;
-            const uint32_t nbytes =
-                left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
-            cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16,
-                        p.x + m * p.ldx + (nbytes ? k : 0), nbytes);
+        if constexpr (LY::kXPrep) {
+          if (lane == 0 && xbytes) {
+            bulk_g2s(st + LY::kWBytes,
+                     reinterpret_cast<const uint8_t*>(p.xperm) +
+                         static_cast<long long>(kt) * kXTileBytes,
+                     xbytes, fb, policy_evict_last());
           }
-          cp_async_mbar_arrive(fb);
-        } else {  // unaligned activations: plain loads, then a regular arrival
-          for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
-            const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
-            unsigned short* xr =
-                reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
-            xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e)
-                                      : static_cast<unsigned short>(0);
+        } else {
+          const long long k0 = static_cast<long long>(kt) * T::kTK;
+          if (p.dry == 4) {  // profiling: stream weights only
+            mbar_arrive(fb);
+          } else if (x_vec) {
+            for (int u = lane; u < units; u += 32) {
+              const int m = u / kXUnits, q = u - m * kXUnits;
+              const long long k = k0 + q * 8;
+              const long long left = p.cols - k;
+              const uint32_t nb =
+                  left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
+              cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16,
+                          p.x + m * p.ldx + (nb ? k : 0), nb);
+            }
+            cp_async_mbar_arrive(fb);
+          } else {  // unaligned activations: plain loads, then a regular arrival
+            for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
+              const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
+              unsigned short* xr =
+                  reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
+              xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e)
+                                        : static_cast<unsigned short>(0);
+            }
+            __threadfence_block();
+            mbar_arrive(fb);
           }
-          __threadfence_block();
-          mbar_arrive(fb);
         }
         if (++stage == kStages) stage = 0, phase ^= 1u;
       }
@@ -461,7 +536,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
       first = false;
       const uint8_t* st = smem + stage * LY::kStageBytes;
       const uint8_t* wt = wlane + stage * LY::kStageBytes;
-      if (p.dry == 1) {
+      if (p.dry == 1 || p.dry == 4) {
         // profiling mode: stream only
       } else if (nk == kChunk) {
         // common case: guard-free and fully unrolled so the loads of the second k-tile
@@ -564,6 +639,25 @@ static cudaError_t launch_linear_m(const LinearParams& p, int grid, cudaStream_t
 
 template <int SCHEME, int NB>
 static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t s) {
+  if constexpr (NB == 2) {
+  // activations first (PDL-chained: waits for whoever produced x, lets the linear start
+  // streaming weights as soon as it is scheduled)
+  const int MS = 8 * NB;
+  const int items = p.k_tiles * MS * 4;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((items + 255) / 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_xprep_kernel<SCHEME>, p.x, p.ldx, p.cols,
+                                     p.M, MS, p.k_tiles, p.xperm);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  }
   if (p.dry == 2) return launch_linear_m<SCHEME, NB, 1>(p, grid, s);  // profiling: no MMA
   if (p.dry == 3) return launch_linear_m<SCHEME, NB, 2>(p, grid, s);  // profiling: no decode
   return launch_linear_m<SCHEME, NB, 0>(p, grid, s);

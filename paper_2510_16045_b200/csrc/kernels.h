@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector_types.h>
 
 namespace amsqb {
 
@@ -29,6 +30,7 @@ struct LinearParams {
   const uint8_t* w;
   const unsigned short* scales;
   const unsigned short* x;  // [M][ldx] fp16 (logical cols)
+  uint2* xperm;             // workspace: x in B-fragment order, [k_tiles][J][8*NB][4] units
   unsigned short* y;        // [M][ldy] fp16
   float* partials;          // [(grid + row_blocks)][16][256] fp32
   int* counters;            // [row_blocks][8 32-row slices], zero between launches
