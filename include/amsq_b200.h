@@ -144,6 +144,12 @@ int amsq_restore_f32(amsq_weight_t h, float* d_out, void* stream);
 /* restore_matrix_half (kernels.hpp:127-133): fp16(w*s), [rows][cols]. Bit-exact. */
 int amsq_restore_f16(amsq_weight_t h, uint16_t* d_out, void* stream);
 
+/* The three restores above into a HOST buffer (device scratch + D2H inside; synchronous):
+ * what = AMSQ_RESTORE_GRID (u16 [rows][padded_cols]), AMSQ_RESTORE_F32 (f32 [rows][cols]) or
+ * AMSQ_RESTORE_F16 (u16 [rows][cols]); bytes must equal that size. */
+enum { AMSQ_RESTORE_GRID = 0, AMSQ_RESTORE_F32 = 1, AMSQ_RESTORE_F16 = 2 };
+int amsq_restore_to_host(amsq_weight_t h, int what, void* host_out, size_t bytes, void* stream);
+
 /* gemv (kernels.hpp:151-187): y[b][r] = fp16(sum_i w_i s_r x_b,i), fp32 accumulation.
  * d_x is [batch][cols] fp16 (logical cols), d_y is [batch][rows] fp16.
  * batch >= 1 (check_gemv_shapes, kernels.hpp:137-143 -> AMSQ_EINVAL). */

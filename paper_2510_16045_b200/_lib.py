@@ -79,6 +79,7 @@ SIGNATURES = {
     "amsq_restore_grid_f16": (_I, [_P, _P, _P]),
     "amsq_restore_f32": (_I, [_P, _P, _P]),
     "amsq_restore_f16": (_I, [_P, _P, _P]),
+    "amsq_restore_to_host": (_I, [_P, _I, _P, _SZ, _P]),
     "amsq_linear": (_I, [_P, _P, _SZ, _P, _P]),
     "amsq_linear_ld": (_I, [_P, _P, _SZ, _P, _SZ, _P]),
     "amsq_gemv_host": (_I, [_P, _U16P, _SZ, _SZ, _U16P, _P]),

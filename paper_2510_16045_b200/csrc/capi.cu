@@ -441,6 +441,30 @@ int amsq_restore_f16(amsq_weight_t h, uint16_t* d_out, void* stream) {
   });
 }
 
+int amsq_restore_to_host(amsq_weight_t h, int what, void* host_out, size_t bytes, void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    if (!host_out) throw amsqb::InvalidArgument("restore_to_host: null output");
+    const auto& L = h->L;
+    size_t need = 0;
+    if (what == AMSQ_RESTORE_GRID) need = L.rows * L.padded_cols * 2;
+    else if (what == AMSQ_RESTORE_F32) need = L.rows * L.cols * 4;
+    else if (what == AMSQ_RESTORE_F16) need = L.rows * L.cols * 2;
+    else throw amsqb::InvalidArgument("restore_to_host: unknown output kind");
+    if (bytes != need) throw amsqb::InvalidArgument("restore_to_host: output size mismatch");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = as_stream(stream);
+    void* d = nullptr;
+    ck(cudaMallocAsync(&d, need, st), "cudaMallocAsync(restore)");
+    restore_impl(h, what == AMSQ_RESTORE_GRID ? static_cast<uint16_t*>(d) : nullptr,
+                 what == AMSQ_RESTORE_F32 ? static_cast<float*>(d) : nullptr,
+                 what == AMSQ_RESTORE_F16 ? static_cast<uint16_t*>(d) : nullptr, st);
+    ck(cudaMemcpyAsync(host_out, d, need, cudaMemcpyDeviceToHost, st), "D2H restore");
+    ck(cudaFreeAsync(d, st), "cudaFreeAsync");
+    ck(cudaStreamSynchronize(st), "restore sync");
+  });
+}
+
 int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream) {
   return guarded([&] {
     check_handle(h);

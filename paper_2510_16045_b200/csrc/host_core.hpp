@@ -3,7 +3,7 @@
 // Scheme/format metadata, the reference packed-stream codec, the host quantizer
 // (RTN + Adaptive Searching, which the north star keeps on the host) and the AMSQ
 // container. Everything here is bit-identical to the reference
-// (/root/reference/proj/include/amsq) -- tests/test_host_core.py checks it against
+// (/root/reference/proj/include/amsq) -- tests/test_host.py checks it against
 // the oracle and the compiled reference -- but is written fresh around flat
 // constexpr tables instead of the reference's cached runtime tables.
 #pragma once

@@ -170,3 +170,17 @@ def test_reference_call_shapes(cuda, orc):
     m = amsq.restore_matrix(qt)
     want = orc.restore_matrix(4, 70, 130, qt.padded_cols, qt.scales, qt.payload)
     assert np.array_equal(m.view(np.uint32), want.view(np.uint32))
+
+
+def test_cpp_dropin_against_reference(cuda):
+    """The reference's own QuantizedTensor / gemv / restore_matrix(_half) next to
+    include/amsq_b200.hpp (tests/cpp/dropin_test.cpp, prebuilt into oracle/_ref)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                       "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test was not built where /root/reference exists")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "0 failure(s)" in r.stdout

@@ -259,3 +259,17 @@ def test_device_entry_points_fail_loudly_without_gpu():
     h = C.c_void_p(None)
     rc = lib().amsq_linear(h, None, 1, None, None)
     assert rc != 0
+
+
+def test_cpp_dropin_without_gpu():
+    """tests/cpp/dropin_test.cpp (reference headers + include/amsq_b200.hpp): without a
+    GPU every device call raises std::runtime_error and shape errors invalid_argument."""
+    import subprocess
+    import torch
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test not built (no /root/reference here)")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: the GPU suite runs this binary")
+    r = subprocess.run([exe, "--no-gpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr

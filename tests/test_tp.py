@@ -1,0 +1,112 @@
+"""Column-parallel TP host logic, world size 2 over gloo on CPU.
+
+Each rank takes its row shard (paper_2510_16045_b200.tp.shard_tensor), computes its
+[M][N/P] output, all-gathers, and un-shards to [M][N]. The result must equal the
+full single-device reference output bit for bit, because a row shard of the reference
+stream produces exactly the matching slice of the reference output. On CPU the local
+compute is the oracle (test infrastructure); the device path (K2 + amsq_tp_unshard) is
+covered by the GPU test at the bottom.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_16045_b200 import tp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, sid, rows, cols, batch, result_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import gaussian_x, quantized_gaussian
+    from oracle import COracle
+    orc = COracle()
+    qt = quantized_gaussian(sid, rows, cols, seed=5)  # same bytes on every rank
+    x = gaussian_x(batch, cols, seed=6)
+    shard = tp.shard_tensor(qt, world, rank)
+    y_local = orc.gemv(sid, shard.rows, cols, qt.padded_cols, shard.scales, shard.payload, x,
+                       batch)  # [M][N/P] fp16 bits
+    # gloo has no 16-bit integer collectives: the fp16 bit patterns travel widened to int32
+    local = torch.from_numpy(y_local.astype(np.int32).reshape(-1))
+    gathered = torch.empty(world * local.numel(), dtype=torch.int32)
+    dist.all_gather_into_tensor(gathered, local)
+    y = tp.unshard_host(gathered.numpy().astype(np.uint16), world, batch, shard.rows)
+    if rank == 0:
+        full = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+        np.save(os.path.join(result_dir, "ok.npy"), np.array([np.array_equal(y, full)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sid,rows,cols,batch", [(7, 64, 200, 3), (4, 96, 256, 5)])
+def test_tp_world2_gloo_matches_single_device(tmp_path, sid, rows, cols, batch):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, sid, rows, cols, batch, str(tmp_path)), nprocs=2, join=True)
+    assert bool(np.load(tmp_path / "ok.npy")[0])
+
+
+def test_shard_range_and_tensor():
+    assert tp.shard_range(8192, 8, 3) == (3072, 1024)
+    assert tp.shard_range(57344, 8, 7) == (50176, 7168)  # 70B gate_up, last rank
+    with pytest.raises(ValueError):
+        tp.shard_range(100, 3, 0)
+    with pytest.raises(ValueError):
+        tp.shard_range(64, 2, 2)
+    from helpers import random_payload
+    qt = random_payload(7, 64, 100, seed=2)
+    parts = [tp.shard_tensor(qt, 4, r) for r in range(4)]
+    assert np.array_equal(np.concatenate([p.payload for p in parts]), qt.payload)
+    assert np.array_equal(np.concatenate([p.scales for p in parts]), qt.scales)
+    assert all(p.padded_cols == qt.padded_cols and p.rows == 16 for p in parts)
+
+
+def test_unshard_host_permutation():
+    P, M, n = 3, 2, 4
+    g = np.arange(P * M * n).reshape(P, M, n)
+    y = tp.unshard_host(g, P, M, n)
+    for p in range(P):
+        assert np.array_equal(y[:, p * n:(p + 1) * n], g[p])
+
+
+@pytest.mark.gpu
+def test_tp_device_path_world1_and_unshard_kernel(cuda, orc):
+    """World size 1 ShardedLinear == full linear; amsq_tp_unshard == unshard_host."""
+    from helpers import check_linear, gaussian_x, quantized_gaussian
+    from paper_2510_16045_b200._lib import check, lib
+    sid, rows, cols, batch = 7, 512, 1000, 4
+    qt = quantized_gaussian(sid, rows, cols, seed=3)
+    x = gaussian_x(batch, cols, seed=4)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = tp.ShardedLinear(qt, device=0)(xt).cpu().numpy().view(np.uint16)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+    # P shard outputs computed on one device, gathered by hand, un-sharded by the kernel
+    P = 4
+    outs = []
+    for r in range(P):
+        row0, n = tp.shard_range(rows, P, r)
+        from paper_2510_16045_b200 import DeviceWeight
+        outs.append(DeviceWeight(qt, device=0, row0=row0, nrows=n).linear(xt))
+    gathered = torch.stack(outs).contiguous()  # [P][M][N/P]
+    out = torch.empty(batch, rows, dtype=torch.float16, device=cuda)
+    check(lib().amsq_tp_unshard(gathered.data_ptr(), P, batch, rows // P, out.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream), "unshard")
+    want = tp.unshard_host(gathered.cpu().numpy(), P, batch, rows // P)
+    assert np.array_equal(out.cpu().numpy(), want)
+    check_linear(out.cpu().numpy().view(np.uint16), yref, yabs)
