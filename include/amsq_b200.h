@@ -98,6 +98,10 @@ int amsq_container_read(const uint8_t* in, size_t in_bytes, int* scheme_id, size
 /* ---- the device tile layout on the host: exposed so the layout and its
  * exact inverse can be checked without a GPU. tiles must hold amsq_device_layout_bytes(). */
 size_t amsq_device_layout_bytes(int scheme_id, size_t rows, size_t cols);
+/* The work plan the layout is built for: plan[4] = {n_groups, g_big, n_big, csplit}
+ * (row tiles split into n_groups contiguous groups, the first n_big of g_big tiles, the
+ * rest of g_big - 1; csplit CTAs per group split K). */
+int amsq_device_layout_plan(int scheme_id, size_t rows, size_t cols, int* plan);
 int amsq_repack(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
                 const uint16_t* payload, size_t payload_words, uint8_t* tiles, size_t tile_bytes);
 int amsq_unrepack(int scheme_id, size_t rows, size_t cols, size_t padded_cols,
@@ -131,6 +135,7 @@ typedef struct {
   size_t device_bytes;         /* bytes of the device tile layout (>= payload_bytes) */
   size_t row_tiles, k_tiles;   /* 16-row x (64|48)-col tiles */
   int device;
+  int n_groups, g_big, n_big, csplit; /* work plan: row groups (one CTA or CTA pair each) */
 } amsq_weight_info_t;
 int amsq_weight_info(amsq_weight_t h, amsq_weight_info_t* out);
 
@@ -178,11 +183,9 @@ int amsq_tp_unshard(const uint16_t* d_gathered, size_t nranks, size_t batch, siz
 
 /* Number of this library's kernels launched so far in this process (bench accounting). */
 uint64_t amsq_kernel_launch_count(void);
-/* Profiling knob: when on, the fused linear streams its operands but skips decode/MMA
- * (results are garbage). Used by tools/prof_linear.py to separate memory and compute. */
-void amsq_debug_set_dry_run(int on);
-/* Profiling knob: device buffer of >= 8 u64 per CTA receiving %globaltimer stamps
- * (start, first stage landed, stream done, end) of each fused-linear CTA; NULL = off. */
+/* Profiling knob: device buffer of >= 64 u64 per CTA receiving %globaltimer stamps of
+ * each fused-linear CTA (0 start, 1 first stage landed, 2 stream done, 3 end, 4..7 the
+ * producer's first issues, 8+2s / 9+2s stage s landed / consumed); NULL = off. */
 void amsq_debug_set_trace(void* d_buf);
 
 #ifdef __cplusplus

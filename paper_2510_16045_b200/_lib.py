@@ -44,7 +44,8 @@ class WeightInfo(C.Structure):
     _fields_ = [("scheme_id", C.c_int), ("rows", C.c_size_t), ("cols", C.c_size_t),
                 ("padded_cols", C.c_size_t), ("payload_bytes", C.c_size_t),
                 ("device_bytes", C.c_size_t), ("row_tiles", C.c_size_t),
-                ("k_tiles", C.c_size_t), ("device", C.c_int)]
+                ("k_tiles", C.c_size_t), ("device", C.c_int), ("n_groups", C.c_int),
+                ("g_big", C.c_int), ("n_big", C.c_int), ("csplit", C.c_int)]
 
 
 # Every symbol include/amsq_b200.h declares, with (restype, argtypes).
@@ -67,6 +68,7 @@ SIGNATURES = {
     "amsq_container_read": (_I, [_U8P, _SZ, C.POINTER(C.c_int), C.POINTER(_SZ), C.POINTER(_SZ),
                                  C.POINTER(_SZ), _U16P, _SZ, _U16P, _SZ]),
     "amsq_device_layout_bytes": (_SZ, [_I, _SZ, _SZ]),
+    "amsq_device_layout_plan": (_I, [_I, _SZ, _SZ, _P]),
     "amsq_repack": (_I, [_I, _SZ, _SZ, _SZ, _U16P, _SZ, _U8P, _SZ]),
     "amsq_unrepack": (_I, [_I, _SZ, _SZ, _SZ, _U8P, _SZ, _U16P, _SZ]),
     "amsq_weight_upload": (_I, [_I, _SZ, _SZ, _SZ, _U16P, _U16P, _SZ, _I, _P, C.POINTER(_P)]),
@@ -86,7 +88,6 @@ SIGNATURES = {
     "amsq_linear_tp": (_I, [_P, _P, _SZ, _P, _P, _SZ, _P, _I, _P]),
     "amsq_tp_unshard": (_I, [_P, _SZ, _SZ, _SZ, _P, _P]),
     "amsq_kernel_launch_count": (C.c_uint64, []),
-    "amsq_debug_set_dry_run": (None, [_I]),
     "amsq_debug_set_trace": (None, [_P]),
 }
 

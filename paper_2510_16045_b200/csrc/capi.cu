@@ -23,15 +23,13 @@ struct amsq_weight_s {
   int device = 0;
   uint8_t* d_w = nullptr;
   unsigned short* d_scales = nullptr;
-  float* d_partials = nullptr;
-  int* d_counters = nullptr;
   uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 16 batch rows)
+  unsigned short* d_xk = nullptr;  // K3 activation image (<= 256 batch rows), lazily allocated
 };
 
 namespace {
 
 thread_local std::string g_error;
-int g_dry_run = 0;  // amsq_debug_set_dry_run(): profiling knob, never set by the product
 unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
 
 struct CudaError : std::runtime_error {
@@ -110,6 +108,10 @@ struct DeviceGuard {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+amsqb::GroupPlan plan_of(const amsqb::DeviceLayout& L) {
+  return amsqb::GroupPlan{L.n_groups, L.g_big, L.n_big, L.csplit};
+}
+
 void check_handle(amsq_weight_t h) {
   if (!h || !h->d_w) throw amsqb::InvalidArgument("null weight handle");
 }
@@ -133,17 +135,12 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   amsqb::repack_to_device(h->L, payload + row0 * wpr, tiles.data(), 0);
   std::vector<unsigned short> sc(h->L.row_tiles * 16, 0);
   std::memcpy(sc.data(), scales + row0, nrows * sizeof(uint16_t));
-  const size_t grid = static_cast<size_t>(amsqb::kMaxGridCTAs);
-  const size_t partial_floats = (grid + h->L.row_blocks()) * 16 * 256;
   cudaStream_t st = as_stream(stream);
   ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");
   ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
-  ck(cudaMalloc(&h->d_partials, partial_floats * sizeof(float)), "cudaMalloc(partials)");
-  ck(cudaMalloc(&h->d_counters, h->L.row_blocks() * 8 * sizeof(int)), "cudaMalloc(counters)");
   ck(cudaMalloc(&h->d_xperm, h->L.k_tiles * 4 * 16 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
   ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
   ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
-  ck(cudaMemsetAsync(h->d_counters, 0, h->L.row_blocks() * 8 * sizeof(int), st), "memset counters");
   ck(cudaStreamSynchronize(st), "upload sync");  // host staging buffers die here
   return h.release();
 }
@@ -153,9 +150,8 @@ void free_impl(amsq_weight_t h) {
   DeviceGuard dg(h->device);
   cudaFree(h->d_w);
   cudaFree(h->d_scales);
-  cudaFree(h->d_partials);
-  cudaFree(h->d_counters);
   cudaFree(h->d_xperm);
+  cudaFree(h->d_xk);
   delete h;
 }
 
@@ -170,17 +166,42 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.scheme_id = h->L.scheme_id;
   p.w = h->d_w;
   p.scales = h->d_scales;
-  p.partials = h->d_partials;
-  p.counters = h->d_counters;
   p.xperm = h->d_xperm;
   p.rows = static_cast<long long>(h->L.rows);
   p.cols = static_cast<long long>(h->L.cols);
   p.ldx = p.cols;
   p.ldy = static_cast<long long>(ldy);
-  p.row_blocks = static_cast<int>(h->L.row_blocks());
+  p.row_tiles = static_cast<int>(h->L.row_tiles);
   p.k_tiles = static_cast<int>(h->L.k_tiles);
-  p.dry = g_dry_run;
+  p.plan = plan_of(h->L);
   p.trace = g_trace;
+  if (batch > static_cast<size_t>(amsqb::linear_max_batch_per_launch())) {
+    // K3: tcgen05 tiles, up to 256 batch rows per launch (weights streamed once per launch)
+    if (!h->d_xk) {
+      ck(cudaMalloc(&h->d_xk, static_cast<size_t>(amsqb::kTcMaxBatch) * h->L.k_tiles * h->L.tk * 2),
+         "cudaMalloc(xk)");
+    }
+    amsqb::TcParams q{};
+    q.scheme_id = h->L.scheme_id;
+    q.w = h->d_w;
+    q.scales = h->d_scales;
+    q.xk = h->d_xk;
+    q.rows = p.rows;
+    q.ldy = p.ldy;
+    q.row_tiles = p.row_tiles;
+    q.k_tiles = p.k_tiles;
+    q.plan = p.plan;
+    for (size_t b0 = 0; b0 < batch; b0 += amsqb::kTcMaxBatch) {
+      const size_t mb = batch - b0 < static_cast<size_t>(amsqb::kTcMaxBatch) ? batch - b0 : amsqb::kTcMaxBatch;
+      q.M = static_cast<int>(mb);
+      q.Np = static_cast<int>((mb + 15) / 16 * 16);
+      q.y = reinterpret_cast<unsigned short*>(d_y) + b0 * ldy;
+      ck(amsqb::launch_linear_tc(q, reinterpret_cast<const unsigned short*>(d_x) + b0 * h->L.cols,
+                                 p.cols, p.cols, st),
+         "amsq_linear_tc_kernel launch");
+    }
+    return;
+  }
   const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
   for (size_t b0 = 0; b0 < batch; b0 += step) {
     const size_t mb = batch - b0 < step ? batch - b0 : step;
@@ -203,6 +224,7 @@ void restore_impl(amsq_weight_t h, uint16_t* grid, float* f32, uint16_t* f16, cu
   p.padded_cols = static_cast<long long>(h->L.padded_cols);
   p.row_tiles = static_cast<int>(h->L.row_tiles);
   p.k_tiles = static_cast<int>(h->L.k_tiles);
+  p.plan = plan_of(h->L);
   p.grid_out = reinterpret_cast<unsigned short*>(grid);
   p.f32_out = f32;
   p.f16_out = reinterpret_cast<unsigned short*>(f16);
@@ -328,6 +350,15 @@ size_t amsq_device_layout_bytes(int id, size_t rows, size_t cols) {
   }
 }
 
+int amsq_device_layout_plan(int id, size_t rows, size_t cols, int* plan) {
+  return guarded([&] {
+    if (!plan) throw amsqb::InvalidArgument("null output");
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    const auto L = amsqb::make_device_layout(id, rows, cols, amsqb::padded_cols(s, cols));
+    plan[0] = L.n_groups, plan[1] = L.g_big, plan[2] = L.n_big, plan[3] = L.csplit;
+  });
+}
+
 int amsq_repack(int id, size_t rows, size_t cols, size_t pc, const uint16_t* payload,
                 size_t words, uint8_t* tiles, size_t tile_bytes) {
   return guarded([&] {
@@ -415,6 +446,10 @@ int amsq_weight_info(amsq_weight_t h, amsq_weight_info_t* out) {
     out->payload_bytes = L.rows * L.wpr * 2;
     out->device_bytes = L.bytes();
     out->row_tiles = L.row_tiles;
+    out->n_groups = L.n_groups;
+    out->g_big = L.g_big;
+    out->n_big = L.n_big;
+    out->csplit = L.csplit;
     out->k_tiles = L.k_tiles;
     out->device = h->device;
   });
@@ -541,7 +576,6 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
 
 uint64_t amsq_kernel_launch_count(void) { return amsqb::kernel_launch_count(); }
 
-void amsq_debug_set_dry_run(int on) { g_dry_run = on; }
 void amsq_debug_set_trace(void* d_buf) { g_trace = static_cast<unsigned long long*>(d_buf); }
 
 }  // extern "C"

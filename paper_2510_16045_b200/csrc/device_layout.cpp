@@ -1,7 +1,9 @@
 // device_layout.cpp -- see device_layout.hpp for the bit map.
 #include "device_layout.hpp"
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "host_core.hpp"
 
@@ -23,10 +25,46 @@ DeviceLayout make_device_layout(int id, size_t rows, size_t cols, size_t pc) {
   L.wpr = words_per_row(s, pc);
   L.tk = id == 4 ? 64 : 48;
   L.tile_bytes = id == 4 ? 544 : 512;
-  const size_t rt = (rows + kRowsPerTile - 1) / kRowsPerTile;
-  L.row_tiles = (rt + kRowTilesPerBlock - 1) / kRowTilesPerBlock * kRowTilesPerBlock;
+  L.row_tiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   L.k_tiles = (pc + L.tk - 1) / L.tk;
+  choose_plan(L.row_tiles, L.k_tiles, &L);
   return L;
+}
+
+// Per-CTA work = G row tiles x ceil(KT / C) k-tiles (G = ceil(RT / n_groups)); pick the
+// plan with the least work per CTA, and among plans within 1 % of it the one that keeps the
+// most SMs streaming (more CTAs = more bytes in flight), then the smaller K split.
+void choose_plan(size_t RT, size_t KT, DeviceLayout* L) {
+  struct Cand {
+    double work;
+    int ctas, C, ng, G;
+  };
+  std::vector<Cand> cands;
+  for (int C = 1; C <= 8; C *= 2) {
+    if (C > 1 && KT < 2 * static_cast<size_t>(C)) continue;
+    const size_t max_groups = std::min<size_t>(RT, kMaxClusters[C]);
+    for (size_t ng = 1; ng <= max_groups; ++ng) {
+      const size_t G = (RT + ng - 1) / ng;
+      if (G > static_cast<size_t>(kMaxGroupTiles) || (RT + G - 1) / G != ng) continue;
+      // a cluster's DSMEM reduction costs about one k-tile of streaming per rank
+      const double work = static_cast<double>(G) *
+                          (static_cast<double>((KT + C - 1) / C) + (C > 1 ? 0.5 * C : 0.0));
+      cands.push_back({work, static_cast<int>(ng) * C, C, static_cast<int>(ng),
+                       static_cast<int>(G)});
+    }
+  }
+  if (cands.empty()) throw InvalidArgument("device layout: no work plan (too many rows per SM)");
+  double best = cands[0].work;
+  for (const Cand& c : cands) best = std::min(best, c.work);
+  const Cand* pick = nullptr;
+  for (const Cand& c : cands) {
+    if (c.work > best * 1.01) continue;
+    if (!pick || c.ctas > pick->ctas || (c.ctas == pick->ctas && c.C < pick->C)) pick = &c;
+  }
+  L->n_groups = pick->ng;
+  L->g_big = pick->G;
+  L->n_big = static_cast<int>(RT - static_cast<size_t>(pick->ng) * (pick->G - 1));
+  L->csplit = pick->C;
 }
 
 namespace {

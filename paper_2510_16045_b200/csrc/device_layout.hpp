@@ -25,11 +25,17 @@
 //      i=2: (mag4>>1)<<4, M1@13, sign@14 | high: (mag4>>1)<<20, M1@29, sign@30
 //      shared: a@12, b@28
 //
-// Tiles are stored [row_block][k_tile][row_tile_in_block] (row block = 16 row tiles =
-// 256 rows): the 16 tiles of one k-tile are contiguous, so a pipeline stage of the fused
-// linear (one row block x kChunk k-tiles) is ONE cp.async.bulk of 16*kChunk tiles --
-// the TMA engine pays a fixed cost per copy, so copies must be large. Row tiles are
-// padded to a multiple of 16, K to a multiple of TK; padding is zero and restores to +0.
+// Work plan and tile order (sm_100a, 148 SMs): the row tiles are split into `n_groups`
+// contiguous row groups of g_big or g_big - 1 tiles (the first n_big groups are the big
+// ones). Each group is processed by one CTA -- or by a cluster of `csplit` = 2/4/8 CTAs that
+// split K and reduce through distributed shared memory -- over the FULL K range, so no
+// partial sums ever leave the SM (cluster). The plan is chosen at upload from (row tiles,
+// k tiles) alone to minimise the per-CTA tile count (SURVEY.md §7 hard part 4), so the
+// fp32 summation order depends only on the shape.
+// Tiles of a group are stored [k_tile][row_tile_in_group]: a CTA's whole weight range is
+// one contiguous region and a pipeline stage (S k-tiles x G row tiles) is ONE
+// cp.async.bulk. Padding rows (to a multiple of 16) and columns (to a multiple of TK)
+// are zero and restore to +0.
 #pragma once
 
 #include <cstddef>
@@ -37,26 +43,47 @@
 
 namespace amsqb {
 
+constexpr int kPlanSMs = 148;   // B200 SM count the plan is built for
+// Clusters of C CTAs that can be co-resident (C = 1, 2, 4, 8; index by C). Larger clusters
+// must fit inside one GPC, which strands SMs: 4 -> 32 clusters, 8 -> 16 clusters assumed
+// (conservative; tools/cluster_probe reports the device's own figure).
+constexpr int kMaxClusters[9] = {0, 148, 74, 0, 32, 0, 0, 0, 16};
+constexpr int kMaxGroupTiles = 64;  // 16 consumer warps x 4 row tiles each
+
 struct DeviceLayout {
   int scheme_id = -1;
   size_t rows = 0, cols = 0, padded_cols = 0;
   size_t wpr = 0;        // reference words per row
   size_t tk = 0;         // columns per k-tile
   size_t tile_bytes = 0;
-  size_t row_tiles = 0;  // padded to a multiple of kRowTilesPerBlock
+  size_t row_tiles = 0;  // ceil(rows / 16)
   size_t k_tiles = 0;
-  size_t row_blocks() const { return row_tiles / 16; }
+  // plan
+  int n_groups = 0, g_big = 0, n_big = 0, csplit = 1;
+  int ctas() const { return n_groups * csplit; }
+  size_t group_row0(size_t g) const {
+    return g < static_cast<size_t>(n_big) ? g * g_big
+                                          : n_big * static_cast<size_t>(g_big) +
+                                                (g - n_big) * static_cast<size_t>(g_big - 1);
+  }
+  size_t group_size(size_t g) const { return g < static_cast<size_t>(n_big) ? g_big : g_big - 1; }
+  size_t group_of(size_t rt) const {
+    const size_t big_rows = static_cast<size_t>(n_big) * g_big;
+    return rt < big_rows ? rt / g_big : n_big + (rt - big_rows) / (g_big - 1);
+  }
   size_t bytes() const { return row_tiles * k_tiles * tile_bytes; }
   size_t tile_offset(size_t rt, size_t kt) const {
-    return ((rt / 16 * k_tiles + kt) * 16 + rt % 16) * tile_bytes;
+    const size_t g = group_of(rt), r0 = group_row0(g);
+    return (r0 * k_tiles + kt * group_size(g) + (rt - r0)) * tile_bytes;
   }
 };
 
 constexpr size_t kRowsPerTile = 16;
-constexpr size_t kRowTilesPerBlock = 16;  // 256-row blocks (8 warps x 2 row tiles)
 
 bool device_scheme_supported(int scheme_id);
 DeviceLayout make_device_layout(int scheme_id, size_t rows, size_t cols, size_t padded_cols);
+// The plan for (row tiles, k tiles): fills n_groups, g_big, n_big, csplit.
+void choose_plan(size_t row_tiles, size_t k_tiles, DeviceLayout* L);
 
 // payload: reference rows [rows][wpr] (row-major). out: layout.bytes() bytes.
 void repack_to_device(const DeviceLayout& L, const uint16_t* payload, uint8_t* out, int threads);

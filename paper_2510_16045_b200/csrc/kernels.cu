@@ -38,10 +38,23 @@ __global__ void __launch_bounds__(128) amsq_restore_kernel(RestoreParams p) {
   const long long tile = static_cast<long long>(blockIdx.x) * 4 + warp;
   const long long ntiles = static_cast<long long>(p.row_tiles) * p.k_tiles;
   if (tile >= ntiles) return;
-  // tiles are enumerated in storage order [row_block][k_tile][row_tile_in_block]
-  const long long rbk = tile / 16;
-  const int rt = static_cast<int>(rbk / p.k_tiles) * 16 + static_cast<int>(tile % 16);
-  const int kt = static_cast<int>(rbk % p.k_tiles);
+  // tiles are enumerated in storage order [group][k_tile][row_tile_in_group]
+  const GroupPlan& P = p.plan;
+  const long long KT = p.k_tiles;
+  const long long big_tiles = static_cast<long long>(P.n_big) * P.g_big * KT;
+  long long G, grp, rem;
+  if (tile < big_tiles) {
+    G = P.g_big;
+    grp = tile / (G * KT);
+    rem = tile - grp * G * KT;
+  } else {
+    G = P.g_big - 1;
+    const long long t2 = tile - big_tiles;
+    grp = P.n_big + t2 / (G * KT);
+    rem = t2 - (grp - P.n_big) * G * KT;
+  }
+  const int kt = static_cast<int>(rem / G);
+  const int rt = P.row0(static_cast<int>(grp)) + static_cast<int>(rem - kt * G);
   const uint8_t* src = p.w + tile * T::kTileBytes;
   const uint4 v = *reinterpret_cast<const uint4*>(src + lane * 16);
   const uint32_t R[4] = {v.x, v.y, v.z, v.w};
@@ -136,460 +149,357 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 }
 
 // =====================================================================================
-// K2: fused restore + linear, M <= 8*NB (NB = 1 or 2).
+// K2: fused restore + linear, M <= 8*NB per launch (NB = 1 or 2).
 //
-// Warp-specialised persistent CTA (one per SM): warp 8 is the producer -- its lane 0
-// streams, per pipeline stage, kChunk k-tiles of the CTA's 16 row tiles (one
-// cp.async.bulk per row tile) plus the matching activation rows (natural layout, one
-// bulk copy per batch row, zero-filled past `cols`) into a 4-deep ring guarded by
-// full/empty mbarriers. Warps 0..7 are consumers: warp w owns row tiles 2w, 2w+1,
-// decodes its 16 B per tile in registers, gathers B fragments with PRMT and issues
-// m16n8k16 MMAs (fp32 accumulation). Units are (256-row block, k-tile) pairs split
-// evenly over the grid (stream-K); a row block cut between CTAs is finished by the
-// last contributor, which sums the fp32 partials in CTA order (deterministic).
+// One CTA (or a cluster of CS = 2/4/8 CTAs splitting K) per row group of the weight's plan
+// (device_layout.hpp): the CTA owns G row tiles over its whole K range, so partial sums
+// never leave the SM / cluster and there is no global split-K fix-up.
+//  * warp 16 = producer: per pipeline stage ONE cp.async.bulk of S k-tiles x G row tiles
+//    (contiguous in the [group][k_tile][row_tile] layout) plus the stage's activations
+//    (LDGSTS natural rows for M <= 8, bulk copy of B-fragment units for M <= 16), into a
+//    ring guarded by full/empty mbarriers; weights are requested before griddepcontrol.wait
+//    (they never depend on the previous kernel).
+//  * warps 0..15 = consumers: warp w takes k-slot w / wr of every stage and the row tiles
+//    r = w % wr + i*wr (i < 4); per k-tile it gathers the B fragments once and reuses them
+//    for its row tiles: LDS.128 + in-register decode + m16n8k16 MMAs, fp32 accumulation.
+//  * epilogue: the S k-slot partials are summed in k-slot order through shared memory, the
+//    CTAs of a cluster are summed in rank order through DSMEM, scale * 2^14, fp16 round.
+//    Deterministic: the summation order depends only on the shape.
 // =====================================================================================
-constexpr int kGroupWarps = 8;                   // a consumer group covers a 256-row block
-constexpr int kGroups = 2;                       // groups split every stage's k-tiles
-constexpr int kConsumerWarps = kGroups * kGroupWarps;
+constexpr int kConsumerWarps = 16;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
-constexpr int kChunk = 4;    // k-tiles per stage: 32-35 KB bulk copies (>= 16 KB, tools/tma_probe.cu)
-constexpr int kGroupK = kChunk / kGroups;        // k-tiles of a stage each group consumes
-constexpr int kMaxStages = 5;  // ring depth (fewer when the stage is large, see K2Layout);
-                               // a <= 113 KB variant that lets PDL successors co-reside was
-                               // measured slower (too few bytes in flight)
+constexpr int kMaxOwn = 4;                              // row tiles per consumer warp
 
-// One CTA per SM: co-resident CTAs were measured to starve each other at the warp arbiter
-// (the lower-priority CTA finishes ~40% later), so each SM runs a single CTA whose two
-// consumer groups each take half of every stage's k-tiles (balanced at segment ends).
-template <int SCHEME, int NB>
-struct K2Layout {
-  using T = Traits<SCHEME>;
-  static constexpr int kMS = 8 * NB;
-  static constexpr int kWBytes = 16 * kChunk * T::kTileBytes;
-  // Activations of a stage. M <= 8 (NB = 1): natural row-major rows loaded by LDGSTS, the
-  // row stride padded so the lanes' LDS hit distinct banks (96 (mod 128) bytes for the
-  // 24-byte FP5.33 lane runs, 16 (mod 128) for FP4.25) and B fragments gathered with PRMT.
-  // M <= 16 (NB = 2): B-fragment-order units ((kk * J + j) * MS + m) * 4 + t written by
-  // amsq_xprep_kernel and bulk-copied, one conflict-free LDS.64 per MMA.
-  static constexpr bool kXPrep = NB == 2;
-  static constexpr int kXRaw = kChunk * T::kTK * 2;
-  static constexpr int kXTarget = SCHEME == 7 ? 96 : 16;
-  static constexpr int kXRow = kXRaw + ((kXTarget - kXRaw % 128) + 128) % 128;
-  static constexpr int kXBytes = kXPrep ? kChunk * T::kJ * kMS * 4 * 8 : kMS * kXRow;
-  static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kScratchBytes = kGroupWarps * 32 * 2 * NB * 4 * 4;
-  static constexpr int kFit = (227 * 1024 - kScratchBytes - 1024) / kStageBytes;
-  static constexpr int kStages = kFit < kMaxStages ? kFit : kMaxStages;
-  static constexpr int kScratchOff = kStages * kStageBytes;  // group-1 accumulators
-  static constexpr int kBarOff = kScratchOff + kScratchBytes;
-  static constexpr int kBytes = kBarOff + 2 * kStages * 8 + 16;
-  static_assert(kWBytes % 16 == 0 && kStageBytes % 16 == 0, "alignment");
-  static_assert(kBytes <= 227 * 1024, "shared memory budget");
+struct K2Geom {
+  int S, wr;         // k-tiles per stage; warps sharing a k-slot (row-tile interleave)
+  int kpw;           // k-tiles per warp per stage (S = kpw * 16 / wr)
+  int w_stage;       // weight bytes reserved per stage (max group)
+  int x_row;         // natural-layout activation row stride (bytes), M <= 8
+  int xrows;         // natural-layout activation rows held per stage (= M)
+  int stage;         // bytes per stage (weights + activations), 128-aligned
+  int stages;        // ring depth
 };
 
-// Units are (256-row block, k-tile) pairs, u = rb * KT + kt; CTA c owns [start(c), start(c+1)).
-__device__ __forceinline__ int unit_start(int c, int U, int G) {
-  return static_cast<int>(static_cast<long long>(c) * U / G);
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
-// CTA owning unit u: the largest c with unit_start(c) <= u (G <= U: every range non-empty).
-__device__ __forceinline__ int unit_owner(int u, int U, int G) {
-  return static_cast<int>((static_cast<long long>(u + 1) * G - 1) / U);
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
 }
 
-// One k-tile of the consumer loop for a warp's two row tiles: decode, gather the B
-// fragments of every batch block from the natural-layout activations, 2*J*NB MMAs.
-// Activation rows >= M are zero in shared memory, so the loads are unpredicated.
-template <int SCHEME, int NB, int MODE = 0>  // MODE (profiling): 1 = no MMA, 2 = no decode
-__device__ __forceinline__ void consume_ktile(const uint8_t* st, int kk, const uint4 (&wv)[2],
-                                              const uint32_t (&sh)[2], float (&acc)[2][NB][4],
-                                              int g, int t) {
+template <int SCHEME, int NB>
+__device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo, int ks,
+                                           int g, int t, uint32_t (&B)[NB][Traits<SCHEME>::kJ][2]) {
   using T = Traits<SCHEME>;
-  using LY = K2Layout<SCHEME, NB>;
-  constexpr int J = T::kJ;
-  uint32_t A[2][J][4];
-#pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const uint32_t R[4] = {wv[rr].x, wv[rr].y, wv[rr].z, wv[rr].w};
-    if constexpr (MODE == 2) {
-#pragma unroll
-      for (int j = 0; j < J; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) A[rr][j][q] = R[(j + q) & 3] & 0x3F003F00u;
-    } else if constexpr (SCHEME == 4) {
-      decode_s4(R, sh[rr], A[rr]);
-    } else {
-      decode_s7(R, A[rr]);
-    }
-  }
+  constexpr int J = T::kJ, MS = 8 * NB;
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    uint32_t B[J][2];
-    if constexpr (LY::kXPrep) {
-      const uint2* xs = reinterpret_cast<const uint2*>(st + LY::kWBytes) +
-                        ((kk * J) * LY::kMS + nb * 8 + g) * 4 + t;
+    if constexpr (NB == 2) {
+      const uint2* xu = reinterpret_cast<const uint2*>(xs) + ((ks * J) * MS + nb * 8 + g) * 4 + t;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        const uint2 b = xs[j * LY::kMS * 4];
-        B[j][0] = b.x;
-        B[j][1] = b.y;
+        const uint2 b = xu[j * MS * 4];
+        B[nb][j][0] = b.x;
+        B[nb][j][1] = b.y;
       }
     } else {
-      const uint8_t* xp =
-          st + LY::kWBytes + (nb * 8 + g) * LY::kXRow + (kk * T::kTK + t * T::kLaneK) * 2;
+      // batch rows >= M only feed accumulator columns that are never stored: read row M-1
+      const uint8_t* xp = xs + min(g, geo.xrows - 1) * geo.x_row + (ks * T::kTK + t * T::kLaneK) * 2;
       if constexpr (SCHEME == 4) {
         const uint4 a = *reinterpret_cast<const uint4*>(xp);
         const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
         const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        bfrag_s4(w, B);
+        bfrag_s4(w, B[nb]);
       } else {
         const uint2 a = *reinterpret_cast<const uint2*>(xp);
         const uint2 b = *reinterpret_cast<const uint2*>(xp + 8);
         const uint2 d = *reinterpret_cast<const uint2*>(xp + 16);
         const uint32_t w[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
-        bfrag_s7(w, B);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      if constexpr (MODE == 1) {  // keep the decode live without the tensor pipe
-        acc[0][nb][j & 3] += __uint_as_float((A[0][j][0] ^ A[0][j][1] ^ A[0][j][2] ^ A[0][j][3] ^ B[j][0]) & 0x3F0F0F0Fu);
-        acc[1][nb][j & 3] += __uint_as_float((A[1][j][0] ^ A[1][j][1] ^ A[1][j][2] ^ A[1][j][3] ^ B[j][1]) & 0x3F0F0F0Fu);
-      } else {
-        mma16816(acc[0][nb], A[0][j], B[j][0], B[j][1]);
-        mma16816(acc[1][nb], A[1][j], B[j][0], B[j][1]);
+        bfrag_s7(w, B[nb]);
       }
     }
   }
 }
 
-template <int SCHEME, int NB, int MODE>
-__global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams p) {
+template <int SCHEME, int NB, int CS>
+__global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams p, K2Geom geo) {
   using T = Traits<SCHEME>;
-  using LY = K2Layout<SCHEME, NB>;
-  constexpr int TILE = T::kTileBytes;
-  constexpr int MS = 8 * NB;
+  constexpr int TILE = T::kTileBytes, J = T::kJ, TK = T::kTK, MS = 8 * NB, NB4 = NB * 4;
+  constexpr bool kXPrep = NB == 2;
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int kStages = LY::kStages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff);
-  uint64_t* empty = full + kStages;
-  float* scratch = reinterpret_cast<float*>(smem + LY::kScratchOff);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int grp = blockIdx.x / CS;
+  const uint32_t crank = CS > 1 ? cluster_ctarank() : 0u;
+  const int G = p.plan.size(grp), rt0 = p.plan.row0(grp);
   const int KT = p.k_tiles;
-  const int U = p.row_blocks * KT;
-  const int G = gridDim.x;
-  const int c = blockIdx.x;
-  const int u0 = unit_start(c, U, G), u1 = unit_start(c + 1, U, G);
-  const int rb_first = u0 / KT, rb_last = (u1 - 1) / KT;
-  unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
-  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+  const int kper = (KT + CS - 1) / CS;
+  const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
+  const int S = geo.S;
+  const int nst = ke > kb ? (ke - kb + S - 1) / S : 0;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
+  uint64_t* empty = full + geo.stages;
+  unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
+  if (trace && threadIdx.x == 0) {
+    trace[0] = globaltimer();
+    trace[63] = clock64();
+  }
   pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      // the producer's arrive.expect_tx, plus one LDGSTS arrival per producer lane when the
-      // activations are loaded in natural layout
-      mbar_init(&full[s], LY::kXPrep ? 1 : 1 + 32);
+    for (int s = 0; s < geo.stages; ++s) {
+      // arrival 1: the producer's arrive.expect_tx (weights + bulk activations); arrival 2:
+      // after the activations were issued / plain-stored (release of the zero tails)
+      mbar_init(&full[s], 2);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
-  // natural-layout activation rows >= M are never written by the producer: zero them once
-  if constexpr (!LY::kXPrep) {
-    for (int s = 0; s < kStages; ++s) {
-      uint4* xz = reinterpret_cast<uint4*>(smem + s * LY::kStageBytes + LY::kWBytes + p.M * LY::kXRow);
-      const int n16 = (MS - p.M) * LY::kXRow / 16;
-      for (int i = threadIdx.x; i < n16; i += blockDim.x) xz[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  float acc[kMaxOwn][NB][4];
+#pragma unroll
+  for (int i = 0; i < kMaxOwn; ++i)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][nb][e] = 0.0f;
+  const int ks = warp / geo.wr, rl = warp % geo.wr;  // k-slot (2 k-tiles per stage), row lane
+  const int nown = warp < kConsumerWarps && rl < G ? min(kMaxOwn, (G - rl + geo.wr - 1) / geo.wr) : 0;
+
+  // The CTA's K range [kb, ke) is walked from a per-group rotation rho: every CTA reads
+  // the SAME activations, and all of them starting at k = 0 would hammer the same L2
+  // lines (measured: ~1 us per stage at M = 1, ~3 us at M = 8). Logical position q maps to
+  // k-tile kb + (rho + q) mod L; a stage may wrap once (two contiguous runs). The fp32
+  // order stays a function of the shape only.
+  const int L = ke - kb;
+  const int rho = L > 0 ? static_cast<int>(static_cast<long long>(grp) * L / p.plan.n_groups) : 0;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------------ producer
+    const uint64_t pol = policy_evict_first();
+    const uint8_t* wgrp = p.w + static_cast<long long>(rt0) * KT * TILE;
+    // bulk copies need 16-byte aligned rows (cols, ldx multiples of 8, 16-byte aligned x)
+    const bool x_bulk = ((p.cols & 7) == 0) && ((p.ldx & 7) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
+    constexpr uint32_t kXTileBytes = J * MS * 4 * 8;
+    // runs of stage st: [k0, k0 + n0) then [k1, k1 + n1) (n1 = 0 when it does not wrap)
+    auto runs = [&](int st, int& k0, int& n0, int& k1, int& n1) {
+      const int q0 = st * S, nk = min(S, L - q0);
+      const int start = (rho + q0) % L;
+      k0 = kb + start;
+      n0 = min(nk, L - start);
+      k1 = kb;
+      n1 = nk - n0;
+    };
+    // activation bytes of row m that a run [kt, kt + nr) covers (the rest is past `cols`)
+    auto xvalid = [&](int kt, int nr) -> uint32_t {
+      const long long left = p.cols - static_cast<long long>(kt) * TK;
+      return static_cast<uint32_t>(left <= 0 ? 0 : (left >= nr * TK ? nr * TK : left) * 2);
+    };
+    auto issue_w = [&](int st, int sidx) {  // lane 0
+      int k0, n0, k1, n1;
+      runs(st, k0, n0, k1, n1);
+      uint8_t* sp = smem + sidx * geo.stage;
+      const uint32_t wbytes = static_cast<uint32_t>((n0 + n1) * G * TILE);
+      uint32_t xbytes = 0;
+      if constexpr (kXPrep) {
+        xbytes = static_cast<uint32_t>(n0 + n1) * kXTileBytes;
+      } else {
+        if (x_bulk) xbytes = static_cast<uint32_t>(p.M) * (xvalid(k0, n0) + (n1 ? xvalid(k1, n1) : 0u));
+      }
+      // no fence.proxy.async: the empty-barrier acquire already orders the consumers' reads
+      // before this async-proxy write (a proxy fence here serialises the copies: measured)
+      mbar_arrive_expect_tx(&full[sidx], wbytes + xbytes);  // arrival 1 of 2
+      bulk_g2s(sp, wgrp + static_cast<long long>(k0) * G * TILE, static_cast<uint32_t>(n0 * G * TILE),
+               &full[sidx], pol);
+      if (n1) {
+        bulk_g2s(sp + n0 * G * TILE, wgrp + static_cast<long long>(k1) * G * TILE,
+                 static_cast<uint32_t>(n1 * G * TILE), &full[sidx], pol);
+      }
+    };
+    auto issue_x = [&](int st, int sidx) {  // whole warp; ends with arrival 2 of 2
+      int k0, n0, k1, n1;
+      runs(st, k0, n0, k1, n1);
+      uint8_t* xs = smem + sidx * geo.stage + geo.w_stage;
+      if constexpr (kXPrep) {
+        if (lane == 0) {
+          const uint8_t* xp = reinterpret_cast<const uint8_t*>(p.xperm);
+          bulk_g2s(xs, xp + static_cast<long long>(k0) * kXTileBytes, n0 * kXTileBytes, &full[sidx],
+                   policy_evict_last());
+          if (n1) {
+            bulk_g2s(xs + n0 * kXTileBytes, xp + static_cast<long long>(k1) * kXTileBytes,
+                     n1 * kXTileBytes, &full[sidx], policy_evict_last());
+          }
+        }
+      } else {
+        for (int run = 0; run < 2; ++run) {
+          const int kt = run ? k1 : k0, nr = run ? n1 : n0, off = run ? n0 : 0;
+          if (nr == 0) continue;
+          const long long kx = static_cast<long long>(kt) * TK;
+          if (x_bulk) {
+            // rows m < M: one bulk copy each (lane m); the part past `cols` is zeroed with
+            // plain stores (only the final k-tile of K has one)
+            const uint32_t vb = xvalid(kt, nr);
+            const int tail16 = (nr * TK * 2 - static_cast<int>(vb)) / 16;
+            for (int u = lane; u < p.M * tail16; u += 32) {
+              const int m = u / tail16, q = u - m * tail16;
+              *reinterpret_cast<uint4*>(xs + m * geo.x_row + off * TK * 2 + vb + q * 16) =
+                  make_uint4(0, 0, 0, 0);
+            }
+            if (lane < p.M && vb) {
+              bulk_g2s(xs + lane * geo.x_row + off * TK * 2, p.x + lane * p.ldx + kx, vb, &full[sidx],
+                       policy_evict_last());
+            }
+          } else {  // unaligned activations: plain loads
+            const int per_row = nr * TK;
+            for (int u = lane; u < p.M * per_row; u += 32) {
+              const int m = u / per_row, e = u - m * per_row;
+              unsigned short* xr = reinterpret_cast<unsigned short*>(xs + m * geo.x_row) + off * TK;
+              xr[e] = (kx + e < p.cols) ? __ldg(p.x + m * p.ldx + kx + e) : static_cast<unsigned short>(0);
+            }
+          }
+        }
+      }
+      __syncwarp();  // the lanes' plain stores happen-before lane 0's release
+      if (lane == 0) mbar_arrive(&full[sidx]);
+    };
+    // weights of the first ring-full of stages are independent of the previous kernel:
+    // request them before griddepcontrol.wait
+    const int first = min(nst, geo.stages);
+    if (lane == 0) {
+      for (int st = 0; st < first; ++st) issue_w(st, st);
+    }
+    pdl_wait();  // activations may be produced by the previous kernel
+    if (trace && lane == 0) trace[4] = clock64();
+    int sidx = 0;
+    uint32_t ph = 0;
+    for (int st = 0; st < nst; ++st) {
+      if (st >= geo.stages) {
+        mbar_wait(&empty[sidx], ph ^ 1u);
+        if (lane == 0) issue_w(st, sidx);
+      }
+      issue_x(st, sidx);
+      if (trace && lane == 0 && st < 3) trace[5 + st] = clock64();
+      if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+    }
+  } else {
+    // ------------------------------------------------------------------ consumers
+    int sidx = 0;
+    uint32_t ph = 0;
+    for (int st = 0; st < nst; ++st) {
+      mbar_wait(&full[sidx], ph);
+      if (trace && threadIdx.x == 0) {
+        if (st == 0) trace[1] = globaltimer();
+        if (st < 28) trace[8 + 2 * st] = clock64();
+      }
+      const int nk = min(S, L - st * S);
+      const uint8_t* sp = smem + sidx * geo.stage;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {  // the warp's k-tiles of the stage (kpw = 1 or 2)
+        const int kq = geo.kpw * ks + kk;
+        if (kk < geo.kpw && kq < nk && nown > 0) {
+          uint32_t B[NB][J][2];
+          load_bfrag<SCHEME, NB>(sp + geo.w_stage, geo, kq, g, t, B);
+          const uint8_t* tb = sp + (kq * G + rl) * TILE + lane * 16;
+          uint4 wv[kMaxOwn];
+          uint32_t sh[kMaxOwn];
+#pragma unroll
+          for (int i = 0; i < kMaxOwn; ++i) {
+            if (i < nown) {
+              const uint8_t* tp = tb + i * geo.wr * TILE;
+              wv[i] = *reinterpret_cast<const uint4*>(tp);
+              sh[i] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kMaxOwn; ++i) {
+            if (i < nown) {
+              uint32_t A[J][4];
+              const uint32_t R[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
+              if constexpr (SCHEME == 4) {
+                decode_s4(R, sh[i], A);
+              } else {
+                decode_s7(R, A);
+              }
+#pragma unroll
+              for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int j = 0; j < J; ++j) mma16816(acc[i][nb], A[j], B[nb][j][0], B[nb][j][1]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
+      if (trace && threadIdx.x == 0 && st < 28) trace[9 + 2 * st] = clock64();
+      if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+    }
+    if (trace && threadIdx.x == 0) trace[2] = globaltimer();
+  }
+
+  // ------------------------------------------------------------------ epilogue
+  __syncthreads();  // every stage consumed: the ring is free for the reduction
+  const int nslots = S / geo.kpw;               // k-slots (a warp covers kpw k-tiles of a stage)
+  float* red = reinterpret_cast<float*>(smem);  // [nslots][G][32][NB4]
+  const int items = G * 32 * NB4;
+  if (warp < kConsumerWarps) {
+#pragma unroll
+    for (int i = 0; i < kMaxOwn; ++i) {
+      if (i < nown) {
+        float* dst = red + (static_cast<long long>(ks) * G + rl + i * geo.wr) * 32 * NB4 + lane * NB4;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[nb * 4 + e] = acc[i][nb][e];
+      }
     }
   }
   __syncthreads();
-
-  if (warp == kConsumerWarps) {
-    // ------------------------------------------------------------ producer warp
-    // lane 0, per stage: one bulk copy of the 16*nk weight tiles (contiguous in the
-    // [row_block][k_tile][row_tile] layout). Activations: NB = 2 -> one more bulk copy of the
-    // prepped B-fragment units; NB = 1 -> all lanes LDGSTS the natural rows (zero-filled
-    // past `cols`), each lane arriving once on the full barrier when its copies land.
-    const uint64_t pol = policy_evict_first();
-    constexpr uint32_t kXTileBytes = T::kJ * MS * 4 * 8;
-    const bool x_vec = ((p.cols & 7) == 0) && ((p.ldx & 7) == 0) &&
-                       ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
-    constexpr int kXUnits = kChunk * T::kTK * 2 / 16;  // 16-byte units per activation row
-    const int units = p.M * kXUnits;
-    int stage = 0;
-    uint32_t phase = 0;
-    bool waited = false;
-    for (int rb = rb_first; rb <= rb_last; ++rb) {
-      const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
-      const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
-      for (int kt = kt0; kt < kt1; kt += kChunk) {
-        const int nk = min(kChunk, kt1 - kt);
-        mbar_wait(&empty[stage], phase ^ 1u);
-        uint8_t* st = smem + stage * LY::kStageBytes;
-        uint64_t* fb = &full[stage];
-        const uint32_t wbytes = static_cast<uint32_t>(16 * nk * TILE);
-        const uint32_t xbytes =
-            (LY::kXPrep && p.dry != 4) ? static_cast<uint32_t>(nk) * kXTileBytes : 0u;
-        if (lane == 0) {
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(fb, wbytes + xbytes);
-          bulk_g2s(st, p.w + (static_cast<long long>(rb) * KT + kt) * 16LL * TILE, wbytes, fb,
-                   pol);
-        }
-        if (!waited) {  // weights are independent of the previous kernel; activations not
-          pdl_wait();
-          waited = true;
-        }
-        if constexpr (LY::kXPrep) {
-          if (lane == 0 && xbytes) {
-            bulk_g2s(st + LY::kWBytes,
-                     reinterpret_cast<const uint8_t*>(p.xperm) +
-                         static_cast<long long>(kt) * kXTileBytes,
-                     xbytes, fb, policy_evict_last());
-          }
-        } else {
-          const long long k0 = static_cast<long long>(kt) * T::kTK;
-          if (p.dry == 4) {  // profiling: stream weights only
-            mbar_arrive(fb);
-          } else if (x_vec) {
-            for (int u = lane; u < units; u += 32) {
-              const int m = u / kXUnits, q = u - m * kXUnits;
-              const long long k = k0 + q * 8;
-              const long long left = p.cols - k;
-              const uint32_t nb =
-                  left >= 8 ? 16u : (left > 0 ? static_cast<uint32_t>(left) * 2u : 0u);
-              cp_async_16(st + LY::kWBytes + m * LY::kXRow + q * 16,
-                          p.x + m * p.ldx + (nb ? k : 0), nb);
-            }
-            cp_async_mbar_arrive(fb);
-          } else {  // unaligned activations: plain loads, then a regular arrival
-            for (int u = lane; u < p.M * kChunk * T::kTK; u += 32) {
-              const int m = u / (kChunk * T::kTK), e = u - m * (kChunk * T::kTK);
-              unsigned short* xr =
-                  reinterpret_cast<unsigned short*>(st + LY::kWBytes + m * LY::kXRow);
-              xr[e] = (k0 + e < p.cols) ? __ldg(p.x + m * p.ldx + k0 + e)
-                                        : static_cast<unsigned short>(0);
-            }
-            __threadfence_block();
-            mbar_arrive(fb);
-          }
-        }
-        if (++stage == kStages) stage = 0, phase ^= 1u;
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumer warps
-  // group gr = warp / 8 consumes the stages of parity gr (chunks 2j + gr of the CTA's
-  // sequence); warp wg = warp % 8 owns row tiles 2wg, 2wg+1 of the 256-row block.
-  const int gr = warp / kGroupWarps, wg = warp % kGroupWarps;
-  const int g = lane >> 2, t = lane & 3;
-  constexpr int kCons = kConsumerWarps * 32;
-  float acc[2][NB][4];
-  bool waited = false;
-
-  // End of a row-block segment: group 1 hands its accumulators to group 0 through shared
-  // memory (sum order g0 + g1: deterministic). Group 0 then either stores y (the CTA
-  // covered the whole K range) or publishes its 32-row slice as an fp32 partial and takes a
-  // ticket on the slice's counter (release; result consumed after the main loop, when the
-  // last contributor of a slice reduces it in CTA order).
-  int pend_rb0 = -1, pend_t0 = 0, pend_rb1 = -1, pend_t1 = 0;
-  const int rib0 = 32 * wg;
-  float* my_scratch = scratch + (wg * 32 + lane) * (2 * NB * 4);
-  auto finish_segment = [&](int rb, bool full_k) {
-    if (!waited) {  // outputs / workspace may still be in use by the previous kernel
-      pdl_wait();
-      waited = true;
-    }
-    if (gr == 1) {
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) my_scratch[(rr * NB + nb) * 4 + e] = acc[rr][nb][e];
-    }
-    named_bar_sync(1, kCons);
-    if (gr == 0) {
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[rr][nb][e] += my_scratch[(rr * NB + nb) * 4 + e];
-      if (full_k) {
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const long long n = static_cast<long long>(rb) * 256 + rib0 + rr * 16 + g + 8 * h;
-            if (n >= p.rows) continue;
-            const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int m = nb * 8 + 2 * t + e;
-                if (m < p.M) {
-                  p.y[static_cast<long long>(m) * p.ldy + n] =
-                      __half_as_ushort(__float2half_rn(acc[rr][nb][2 * h + e] * sc));
-                }
-              }
-            }
-          }
-        }
-      } else {
-        float* part = p.partials + (static_cast<long long>(c) + rb) * MS * 256;
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int m = nb * 8 + 2 * t + e;
-                part[m * 256 + rib0 + rr * 16 + g + 8 * h] = acc[rr][nb][2 * h + e];
-              }
-        __syncwarp();  // the warp's partial stores happen-before lane 0's release
-        int ticket = 0;
-        if (lane == 0) ticket = atomic_add_acq_rel_gpu(&p.counters[rb * kGroupWarps + wg], 1);
-        if (pend_rb0 < 0) {
-          pend_rb0 = rb, pend_t0 = ticket;
-        } else {
-          pend_rb1 = rb, pend_t1 = ticket;
-        }
-      }
-    }
-    named_bar_sync(1, kCons);  // scratch free for the next segment
-  };
-
-  // Deferred reduction of a 32-row slice whose partials are all published: the slice is
-  // M x 8 float4 outputs, each the CTA-ordered sum of ncon partials. Every lane issues the
-  // loads of all its (output, contributor) pairs before adding, four contributors at a time.
-  auto reduce_slice = [&](int rb) {
-    const int c_first = unit_owner(rb * KT, U, G);
-    const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - c_first + 1;
-    const float4* base = reinterpret_cast<const float4*>(
-        p.partials + (static_cast<long long>(c_first) + rb) * MS * 256 + rib0);
-    const int nout = p.M * 8;  // outputs of the slice (<= 128): lane owns o = lane + 32 i
-    float4 sum[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) sum[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < ncon; c0 += 4) {  // 16 independent loads in flight per lane
-      float4 v[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int o = lane + 32 * i;
-          v[i][j] = (o < nout && c0 + j < ncon)
-                        ? __ldcg(base + ((c0 + j) * MS + (o >> 3)) * 64 + (o & 7))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (c0 + j < ncon) {  // contributor order c0, c0+1, ... : deterministic
-            sum[i].x += v[i][j].x, sum[i].y += v[i][j].y, sum[i].z += v[i][j].z,
-                sum[i].w += v[i][j].w;
-          }
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int o = lane + 32 * i;
-      if (o >= nout) continue;
-      const int m = o >> 3, q = o & 7;
-      const float r4[4] = {sum[i].x, sum[i].y, sum[i].z, sum[i].w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const long long n = static_cast<long long>(rb) * 256 + rib0 + 4 * q + e;
-        if (n < p.rows) {
-          const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
-          p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(r4[e] * sc));
-        }
-      }
+  pdl_wait();  // outputs may still be read by the previous kernel
+  float* part = red + static_cast<long long>(nslots) * items;  // [G][32][NB4] (clusters)
+  auto store_y = [&](int it, float v) {
+    const int r = it / (32 * NB4), rem = it - r * 32 * NB4;
+    const int ln = rem / NB4, q = rem - ln * NB4, nb = q >> 2, e = q & 3;
+    const int m = nb * 8 + 2 * (ln & 3) + (e & 1);
+    const long long n = static_cast<long long>(rt0 + r) * 16 + (ln >> 2) + 8 * (e >> 1);
+    if (m < p.M && n < p.rows) {
+      const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+      p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
     }
   };
-
-  int stage = 0;
-  uint32_t phase = 0;
-  bool first = true;
-  const uint8_t* wlane = smem + (2 * wg) * TILE + lane * 16;  // + stage base; [kk][16 row tiles]
-  const int kkb = gr * kGroupK;  // this group's k-tiles of each stage: kkb .. kkb + kGroupK - 1
-  for (int rb = rb_first; rb <= rb_last; ++rb) {
-    const int kt0 = rb == rb_first ? u0 - rb * KT : 0;
-    const int kt1 = rb == rb_last ? u1 - rb * KT : KT;
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[rr][nb][e] = 0.0f;
-    for (int kt = kt0; kt < kt1; kt += kChunk) {
-      const int nk = min(kChunk, kt1 - kt);
-      mbar_wait(&full[stage], phase);
-      if (trace && first && threadIdx.x == 0) trace[1] = globaltimer();
-      first = false;
-      const uint8_t* st = smem + stage * LY::kStageBytes;
-      const uint8_t* wt = wlane + stage * LY::kStageBytes;
-      if (p.dry == 1 || p.dry == 4) {
-        // profiling mode: stream only
-      } else if (nk == kChunk) {
-        // common case: guard-free and fully unrolled so the loads of the second k-tile
-        // overlap the decode/MMA of the first
-        uint4 wv[kGroupK][2];
-        uint32_t sh[kGroupK][2];
-#pragma unroll
-        for (int i = 0; i < kGroupK; ++i)
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const uint8_t* tp = wt + ((kkb + i) * 16 + rr) * TILE;
-            wv[i][rr] = *reinterpret_cast<const uint4*>(tp);
-            sh[i][rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
-          }
-#pragma unroll
-        for (int i = 0; i < kGroupK; ++i)
-          consume_ktile<SCHEME, NB, MODE>(st, kkb + i, wv[i], sh[i], acc, g, t);
-      } else {
-        for (int kk = kkb; kk < min(nk, kkb + kGroupK); ++kk) {
-          uint4 wv[2];
-          uint32_t sh[2];
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const uint8_t* tp = wt + (kk * 16 + rr) * TILE;
-            wv[rr] = *reinterpret_cast<const uint4*>(tp);
-            sh[rr] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
-          }
-          consume_ktile<SCHEME, NB, MODE>(st, kk, wv, sh, acc, g, t);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == kStages) stage = 0, phase ^= 1u;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    float v = 0.0f;
+    for (int k = 0; k < nslots; ++k) v += red[static_cast<long long>(k) * items + it];  // slot order
+    if constexpr (CS == 1) {
+      store_y(it, v);
+    } else {
+      part[it] = v;
     }
-    if (trace && rb == rb_last && threadIdx.x == 0) trace[2] = globaltimer();
-    finish_segment(rb, kt0 == 0 && kt1 == KT);
   }
-  // Slices this warp completed last: reduce them (the acquire in the ticket makes the other
-  // contributors' partials visible to lane 0; __syncwarp extends that to the warp).
-  if (gr == 0) {
+  if constexpr (CS > 1) {
+    cluster_sync_all();  // every CTA's partial visible cluster-wide
+    // rank r finalises row tiles [r*Gs, (r+1)*Gs), summing the CS partials in rank order
+    const int Gs = (G + CS - 1) / CS;
+    const int i0 = min(G, static_cast<int>(crank) * Gs) * 32 * NB4;
+    const int i1 = min(G, static_cast<int>(crank + 1) * Gs) * 32 * NB4;
+    for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
+      float v = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int rb = i == 0 ? pend_rb0 : pend_rb1;
-      if (rb < 0) continue;
-      const int ticket = i == 0 ? pend_t0 : pend_t1;
-      const int ncon = unit_owner((rb + 1) * KT - 1, U, G) - unit_owner(rb * KT, U, G) + 1;
-      const int last = __shfl_sync(0xffffffffu, ticket == ncon - 1 ? 1 : 0, 0);
-      __syncwarp();
-      if (last) {
-        if (lane == 0) store_relaxed_gpu(&p.counters[rb * kGroupWarps + wg], 0);
-        reduce_slice(rb);
-      }
+      for (int r = 0; r < CS; ++r) v += ld_dsmem_f32(part + it, static_cast<uint32_t>(r));
+      store_y(it, v);
     }
+    cluster_sync_all();  // keep our shared memory alive until every peer has read it
   }
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
 }
@@ -599,8 +509,14 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
 // =====================================================================================
 // launchers
 // =====================================================================================
+namespace {
+
+int restore_ntiles(const RestoreParams& p) { return p.row_tiles * p.k_tiles; }
+
+}  // namespace
+
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s) {
-  const long long ntiles = static_cast<long long>(p.row_tiles) * p.k_tiles;
+  const long long ntiles = restore_ntiles(p);
   const unsigned blocks = static_cast<unsigned>((ntiles + 3) / 4);
   if (blocks == 0) return cudaSuccess;
   if (p.scheme_id == 4) {
@@ -612,69 +528,112 @@ cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int SCHEME, int NB, int MODE>
-static cudaError_t launch_linear_m(const LinearParams& p, int grid, cudaStream_t s) {
-  using SM = dev::K2Layout<SCHEME, NB>;
-  static bool configured = false;  // per template instance; attribute is per-function
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes);
+// Stage geometry for a plan: wr = smallest power of two with ceil(G / wr) <= 4 row tiles
+// per consumer warp, S = 16 / wr k-tiles per stage (so a stage is <= 64 tiles, ~32 KB),
+// as many ring stages as fit (<= 6).
+template <int SCHEME, int NB>
+static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
+  // wr = warps sharing a k-slot (row-tile interleave): the smallest power of two giving each
+  // consumer warp <= 2 row tiles (<= 4 beyond 32 tiles); every warp takes 2 k-tiles of each
+  // stage, so a stage is S = 2 * 16 / wr k-tiles x G row tiles (<= 64 tiles, ~32 KB)
+  using T = dev::Traits<SCHEME>;
+  dev::K2Geom geo{};
+  const int G = p.plan.g_big;
+  int wr = 1;
+  while (wr < 16 && (G + wr - 1) / wr > 2) wr *= 2;
+  geo.wr = wr;
+  geo.kpw = NB == 2 ? 1 : 2;  // M <= 16 carries 2x the activation bytes per k-tile
+  geo.S = geo.kpw * (dev::kConsumerWarps / wr);
+  geo.w_stage = (geo.S * G * T::kTileBytes + 127) / 128 * 128;
+  const int x_raw = geo.S * T::kTK * 2;
+  const int target = SCHEME == 7 ? 96 : 16;  // lanes' LDS hit distinct banks
+  geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
+  geo.xrows = NB == 2 ? 16 : p.M;
+  const int x_stage = NB == 2 ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
+  geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
+  const int budget = 227 * 1024 - 1024;
+  geo.stages = budget / geo.stage;
+  if (geo.stages > 6) geo.stages = 6;
+  // the epilogue reuses the ring: (S/kpw + 1) x G x 32 x NB*4 floats
+  const long long red = (static_cast<long long>(geo.S / geo.kpw) + 1) * G * 32 * NB * 4 * 4;
+  while (geo.stages * geo.stage < red) ++geo.stages;
+  *smem_bytes = geo.stages * geo.stage + 2 * geo.stages * 8 + 16;
+  return geo;
+}
+
+template <int SCHEME, int NB, int CS>
+static cudaError_t launch_linear_m(const LinearParams& p, cudaStream_t s) {
+  int smem = 0;
+  const dev::K2Geom geo = k2_geometry<SCHEME, NB>(p, &smem);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  static int configured = 0;  // per template instance; attribute is per-function
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB, CS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured = 227 * 1024;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.gridDim = dim3(static_cast<unsigned>(p.plan.n_groups * CS));
   cfg.blockDim = dim3(dev::kK2Threads);
-  cfg.dynamicSmemBytes = SM::kBytes;
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int na = 1;
+  if constexpr (CS > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CS;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    na = 2;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_kernel<SCHEME, NB, MODE>, p);
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_kernel<SCHEME, NB, CS>, p, geo);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int SCHEME, int NB>
-static cudaError_t launch_linear_t(const LinearParams& p, int grid, cudaStream_t s) {
+static cudaError_t launch_linear_t(const LinearParams& p, cudaStream_t s) {
   if constexpr (NB == 2) {
-  // activations first (PDL-chained: waits for whoever produced x, lets the linear start
-  // streaming weights as soon as it is scheduled)
-  const int MS = 8 * NB;
-  const int items = p.k_tiles * MS * 4;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>((items + 255) / 256));
-  cfg.blockDim = dim3(256);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_xprep_kernel<SCHEME>, p.x, p.ldx, p.cols,
-                                     p.M, MS, p.k_tiles, p.xperm);
-  count_launch();
-  if (e != cudaSuccess) return e;
+    // activations first (PDL-chained: waits for whoever produced x, lets the linear start
+    // streaming weights as soon as it is scheduled)
+    const int MS = 8 * NB;
+    const int items = p.k_tiles * MS * 4;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>((items + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_xprep_kernel<SCHEME>, p.x, p.ldx, p.cols,
+                                       p.M, MS, p.k_tiles, p.xperm);
+    count_launch();
+    if (e != cudaSuccess) return e;
   }
-  if (p.dry == 2) return launch_linear_m<SCHEME, NB, 1>(p, grid, s);  // profiling: no MMA
-  if (p.dry == 3) return launch_linear_m<SCHEME, NB, 2>(p, grid, s);  // profiling: no decode
-  return launch_linear_m<SCHEME, NB, 0>(p, grid, s);
+  switch (p.plan.csplit) {
+    case 1: return launch_linear_m<SCHEME, NB, 1>(p, s);
+    case 2: return launch_linear_m<SCHEME, NB, 2>(p, s);
+    case 4: return launch_linear_m<SCHEME, NB, 4>(p, s);
+    case 8: return launch_linear_m<SCHEME, NB, 8>(p, s);
+    default: return cudaErrorInvalidConfiguration;
+  }
 }
 
 int linear_max_batch_per_launch() { return 16; }
 
-long long linear_grid(long long units, int /*M*/) { return units < kSMs ? units : kSMs; }
-
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {  // NOLINT
-  const long long units = static_cast<long long>(p.row_blocks) * p.k_tiles;
-  const int grid = static_cast<int>(linear_grid(units, p.M));
-  if (grid <= 0) return cudaSuccess;
+  if (p.plan.n_groups <= 0) return cudaSuccess;
   if (p.scheme_id == 4) {
-    return p.M <= 8 ? launch_linear_t<4, 1>(p, grid, s) : launch_linear_t<4, 2>(p, grid, s);
+    return p.M <= 8 ? launch_linear_t<4, 1>(p, s) : launch_linear_t<4, 2>(p, s);
   }
-  return p.M <= 8 ? launch_linear_t<7, 1>(p, grid, s) : launch_linear_t<7, 2>(p, grid, s);
+  return p.M <= 8 ? launch_linear_t<7, 1>(p, s) : launch_linear_t<7, 2>(p, s);
 }
 
 // [P][batch][n] -> [batch][P*n]

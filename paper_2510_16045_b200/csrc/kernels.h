@@ -8,11 +8,15 @@
 
 namespace amsqb {
 
-// Fixed persistent grid of the stream-K linear (one CTA per SM of the 148-SM B200): the
-// split-K partition, and therefore the fp32 reduction order, depends only on the shape,
-// never on the device it runs on.
-constexpr long long kSMs = 148;
-constexpr long long kMaxGridCTAs = kSMs;
+// The row-group plan of a weight (device_layout.hpp): group g covers row tiles
+// [row0(g), row0(g) + size(g)), g_big tiles for g < n_big, g_big - 1 after.
+struct GroupPlan {
+  int n_groups, g_big, n_big, csplit;
+  __host__ __device__ int row0(int g) const {
+    return g < n_big ? g * g_big : n_big * g_big + (g - n_big) * (g_big - 1);
+  }
+  __host__ __device__ int size(int g) const { return g < n_big ? g_big : g_big - 1; }
+};
 
 struct RestoreParams {
   int scheme_id;
@@ -20,6 +24,7 @@ struct RestoreParams {
   const unsigned short* scales;  // fp16 bits [rows]
   long long rows, cols, padded_cols;
   int row_tiles, k_tiles;
+  GroupPlan plan;
   unsigned short* grid_out;  // [rows][padded_cols] grid bits, or null
   float* f32_out;            // [rows][cols] w*s, or null
   unsigned short* f16_out;   // [rows][cols] fp16(w*s), or null
@@ -32,20 +37,33 @@ struct LinearParams {
   const unsigned short* x;  // [M][ldx] fp16 (logical cols)
   uint2* xperm;             // workspace: x in B-fragment order, [k_tiles][J][8*NB][4] units
   unsigned short* y;        // [M][ldy] fp16
-  float* partials;          // [(grid + row_blocks)][16][256] fp32
-  int* counters;            // [row_blocks][8 32-row slices], zero between launches
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
-  int row_blocks, k_tiles;
-  int dry;                  // profiling only: consumers skip decode/MMA (measures the stream)
+  int row_tiles, k_tiles;
+  GroupPlan plan;
   unsigned long long* trace;  // profiling only: per-CTA globaltimer stamps (null = off)
 };
 
+// K3 (kernels_tc.cu): tcgen05 fused linear for 16 < M <= 256 per launch.
+struct TcParams {
+  int scheme_id;
+  const uint8_t* w;
+  const unsigned short* scales;
+  const unsigned short* xk;  // workspace: activations prepped into [K/8][Np][8] (>= Np*KT*TK)
+  unsigned short* y;         // [M][ldy] fp16
+  long long rows, ldy;
+  int M, Np;                 // batch rows; Np = round_up(M, 16) <= 256
+  int row_tiles, k_tiles;
+  GroupPlan plan;
+};
+
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);
+cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
+                             long long cols, cudaStream_t s);
+constexpr int kTcMaxBatch = 256;
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
 cudaError_t launch_unshard(const unsigned short* in, int P, int batch, int n, unsigned short* out,
                            cudaStream_t s);
-long long linear_grid(long long units, int M);
 int linear_max_batch_per_launch();
 uint64_t kernel_launch_count();
 

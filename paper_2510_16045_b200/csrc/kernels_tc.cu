@@ -1,0 +1,392 @@
+// kernels_tc.cu -- K3: fused restore + linear on the 5th-generation tensor cores
+// (tcgen05.mma, TMEM accumulators) for large batches (16 < M <= 256 per launch), where the
+// linear stops being HBM-bound (crossover M ~ 56 / 70).
+//
+// Swap-AB: D[128 weight rows][Np batch] += W[128 x K] . X^T[K x Np], D in TMEM (128 lanes x
+// Np fp32 columns), one CTA per 128-row block (8 row tiles of the tile layout).
+//  * warps 0..7 ("decode"): warp w streams row tile 8*blk + w straight from HBM (one LDG.128
+//    per lane per tile, the next stage prefetched), decodes in registers (the same
+//    decode_s4 / decode_s7 as K2) and stores the placed fp16 pairs into the stage's A
+//    buffer in the UMMA canonical K-major no-swizzle layout [k/8][128 rows][8];
+//    fence.proxy.async + one mbarrier arrival per warp.
+//  * warp 8 ("B producer"): one cp.async.bulk per stage of the activations, prepped once per
+//    call by amsq_xprep_tc_kernel into the same [k/8][Np][8] image; owns the TMEM allocation.
+//  * warp 9 ("MMA"): one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
+//    N=Np, K=16) per 16 columns and tcgen05.commit's the stage back to the producers.
+//  * epilogue (warps 0..7): tcgen05.ld 32x32b -> fp32 * scale * 2^14 -> fp16 y.
+// The decode emits a lane's fp16 pairs in its own order, so the K axis is permuted inside
+// every tile column chunk (tc_kperm); the activation prep applies the same permutation, so
+// the contraction is unchanged. Accumulation order: k ascending per MMA -- deterministic.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "kernels_common.cuh"
+
+namespace amsqb {
+
+void count_launch();
+
+namespace dev {
+
+// Natural column (within a k-tile) of the p-th fp16 a decode lane run emits. A lane (g, t)
+// covers columns [12t, 12t + 12) (FP5.33) / [16t, 16t + 16) (FP4.25) of its rows and emits
+// them as the pairs of decode_s7 / decode_s4 (kernels_common.cuh).
+template <int SCHEME>
+__host__ __device__ __forceinline__ int tc_kperm(int p) {
+  if constexpr (SCHEME == 7) {
+    const int t = p / 12, r = p - 12 * t;
+    const int q = r / 6, i = (r - 6 * q) >> 1, h = r & 1;
+    return 3 * (4 * t + 2 * q + h) + i;
+  } else {
+    const int t = p >> 4, r = p & 15;
+    const int q = r >> 3, j = (r & 7) >> 1, h = r & 1;
+    return 16 * t + 8 * q + 4 * h + j;
+  }
+}
+
+// x[M][ldx] -> xk[KTOT/8][Np][8] (the UMMA no-swizzle K-major image), K permuted per tile.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) amsq_xprep_tc_kernel(const unsigned short* __restrict__ x,
+                                                            long long ldx, long long cols, int M,
+                                                            int Np, int KT,
+                                                            unsigned short* __restrict__ xk) {
+  constexpr int TK = Traits<SCHEME>::kTK;
+  pdl_launch_dependents();
+  pdl_wait();  // x is produced by the previous kernel in the stream
+  const long long total = static_cast<long long>(KT) * TK * Np;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long grp = e / (8LL * Np);
+    const int rem = static_cast<int>(e - grp * 8LL * Np);
+    const int m = rem >> 3, kk = rem & 7;
+    const long long kp = grp * 8 + kk;                // permuted column
+    const long long kt = kp / TK;
+    const long long k = kt * TK + tc_kperm<SCHEME>(static_cast<int>(kp - kt * TK));
+    xk[e] = (m < M && k < cols) ? __ldg(x + m * ldx + k) : static_cast<unsigned short>(0);
+  }
+}
+
+// ---------------------------------------------------------------- tcgen05 helpers
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SM100 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4 [16,30),
+  // SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout SWIZZLE_NONE (0) [61,64)
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) |
+         static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16 |
+         static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32 | 1ull << 46;
+}
+
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+constexpr int kTcDecodeWarps = 8;
+constexpr int kTcThreads = (kTcDecodeWarps + 2) * 32;  // + B producer + MMA issuer
+
+struct TcGeom {
+  int kchunk;   // k-tiles per stage
+  int stages;
+  int a_bytes;  // A buffer per stage: 128 rows x kchunk*TK fp16
+  int b_bytes;  // B buffer per stage: Np rows x kchunk*TK fp16
+  int stage;    // a_bytes + b_bytes (128-aligned)
+  int tmem_cols;
+};
+
+template <int SCHEME>
+__global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams p, TcGeom geo) {
+  using T = Traits<SCHEME>;
+  constexpr int TILE = T::kTileBytes, TK = T::kTK, J = T::kJ;
+  constexpr int RUN = SCHEME == 7 ? 12 : 16;  // columns a lane emits per row and tile
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int blk = blockIdx.x;
+  const int KT = p.k_tiles;
+  const int nst = (KT + geo.kchunk - 1) / geo.kchunk;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
+  uint64_t* fullB = fullA + geo.stages;
+  uint64_t* empty = fullB + geo.stages;
+  uint64_t* done = empty + geo.stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t lboA = 128 * 16, lboB = static_cast<uint32_t>(p.Np) * 16;
+
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < geo.stages; ++s) {
+      mbar_init(&fullA[s], kTcDecodeWarps);
+      mbar_init(&fullB[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == kTcDecodeWarps) {  // TMEM: Np fp32 columns x 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(geo.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kTcDecodeWarps) {
+    // ------------------------------------------------------------------ decode warps
+    const int rt = blk * 8 + warp;
+    const bool live = rt < p.row_tiles;
+    const int g = lane >> 2, t = lane & 3;
+    long long toff[2] = {0, 0};  // not used: tile offsets computed per k-tile
+    (void)toff;
+    const GroupPlan& P = p.plan;
+    int grp = 0, G = 1, r0 = 0;
+    if (live) {
+      const int big_rows = P.n_big * P.g_big;
+      grp = rt < big_rows ? rt / P.g_big : P.n_big + (rt - big_rows) / (P.g_big - 1);
+      G = P.size(grp);
+      r0 = P.row0(grp);
+    }
+    // tile (rt, kt) lives at ((r0 * KT) + kt * G + (rt - r0)) * TILE (device_layout.hpp)
+    const uint8_t* wbase = p.w + (static_cast<long long>(r0) * KT + (rt - r0)) * TILE + lane * 16;
+    const long long kstride = static_cast<long long>(G) * TILE;
+    constexpr int kMaxChunk = 4;
+    uint4 cur[kMaxChunk], nxt[kMaxChunk];
+    uint32_t shc[kMaxChunk], shn[kMaxChunk];
+    auto load_stage = [&](int st, uint4 (&v)[kMaxChunk], uint32_t (&sh)[kMaxChunk]) {
+#pragma unroll
+      for (int kk = 0; kk < kMaxChunk; ++kk) {
+        const int kt = st * geo.kchunk + kk;
+        if (live && kk < geo.kchunk && kt < KT) {
+          const uint8_t* tp = wbase + kt * kstride;
+          v[kk] = __ldcs(reinterpret_cast<const uint4*>(tp));
+          sh[kk] = SCHEME == 4 ? __ldcs(tp + 512 - lane * 16 + lane) : 0u;
+        } else {
+          v[kk] = make_uint4(0, 0, 0, 0);
+          sh[kk] = 0;
+        }
+      }
+    };
+    if (nst > 0) load_stage(0, cur, shc);
+    int sidx = 0;
+    uint32_t ph = 0;
+    for (int st = 0; st < nst; ++st) {
+      if (st + 1 < nst) load_stage(st + 1, nxt, shn);  // prefetch the next stage
+      if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
+      uint8_t* A = smem + sidx * geo.stage;
+#pragma unroll
+      for (int kk = 0; kk < kMaxChunk; ++kk) {
+        if (kk < geo.kchunk && st * geo.kchunk + kk < KT) {
+          uint32_t Af[J][4];
+          const uint32_t R[4] = {cur[kk].x, cur[kk].y, cur[kk].z, cur[kk].w};
+          uint32_t rowg[2 * J], rowg8[2 * J];  // a lane's RUN columns of rows g and g + 8
+          if constexpr (SCHEME == 4) {
+            decode_s4(R, shc[kk], Af);
+            // A[j] = {g:(16t+j,16t+4+j), g+8, g:(16t+8+j,16t+12+j), g+8}: emit q-major
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              rowg[j] = Af[j][0], rowg[4 + j] = Af[j][2];
+              rowg8[j] = Af[j][1], rowg8[4 + j] = Af[j][3];
+            }
+          } else {
+            decode_s7(R, Af);
+            // A[j] = {g: pair 2j, g+8: pair 2j, g: pair 2j+1, g+8: pair 2j+1}
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              rowg[2 * j] = Af[j][0], rowg[2 * j + 1] = Af[j][2];
+              rowg8[2 * j] = Af[j][1], rowg8[2 * j + 1] = Af[j][3];
+            }
+          }
+          // [k/8][128][8] image: column c of row r at (c / 8) * lboA + r * 16 + (c % 8) * 2
+          const int c0 = kk * TK + RUN * t;  // first (permuted) column of the run
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = warp * 16 + g + 8 * h;
+            const uint32_t* v = h ? rowg8 : rowg;
+#pragma unroll
+            for (int q = 0; q < RUN / 4; ++q) {  // 8-byte pieces (4 columns)
+              const int c = c0 + 4 * q;
+              *reinterpret_cast<uint2*>(A + (c >> 3) * lboA + r * 16 + (c & 7) * 2) =
+                  make_uint2(v[2 * q], v[2 * q + 1]);
+            }
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fullA[sidx]);
+#pragma unroll
+      for (int kk = 0; kk < kMaxChunk; ++kk) cur[kk] = nxt[kk], shc[kk] = shn[kk];
+      if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+    }
+  } else if (warp == kTcDecodeWarps) {
+    // ------------------------------------------------------------------ B producer
+    if (lane == 0) {
+      pdl_wait();  // the prepped activations come from the previous kernel
+      int sidx = 0;
+      uint32_t ph = 0;
+      for (int st = 0; st < nst; ++st) {
+        if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
+        const int kt0 = st * geo.kchunk, nk = min(geo.kchunk, KT - kt0);
+        const uint32_t bytes = static_cast<uint32_t>(nk * TK / 8) * lboB;
+        mbar_arrive_expect_tx(&fullB[sidx], bytes);
+        bulk_g2s(smem + sidx * geo.stage + geo.a_bytes,
+                 p.xk + static_cast<long long>(kt0) * TK * p.Np, bytes, &fullB[sidx],
+                 policy_evict_last());
+        if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4)                                      // D: f32
+                             | (static_cast<uint32_t>(p.Np >> 3) << 17)     // N
+                             | (static_cast<uint32_t>(128 >> 4) << 24);     // M
+      int sidx = 0;
+      uint32_t ph = 0;
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(&fullA[sidx], ph);
+        mbar_wait(&fullB[sidx], ph);
+        tc_fence_after();
+        const int nk = min(geo.kchunk, KT - st * geo.kchunk);
+        const uint32_t a0 = smem_u32(smem + sidx * geo.stage);
+        const uint32_t b0 = a0 + geo.a_bytes;
+        for (int k16 = 0; k16 < nk * TK / 16; ++k16) {
+          const uint64_t ad = umma_desc(a0 + k16 * 2 * lboA, lboA, 128);
+          const uint64_t bd = umma_desc(b0 + k16 * 2 * lboB, lboB, 128);
+          tc_mma_f16(tmem, ad, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
+        if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+      }
+      tc_commit(done);
+    }
+  }
+
+  // ------------------------------------------------------------------ epilogue
+  if (warp < kTcDecodeWarps) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    pdl_wait();  // y may still be read by the previous kernel
+    const int quarter = warp & 3, half = warp >> 2;
+    const long long n = static_cast<long long>(blk) * 128 + quarter * 32 + lane;
+    const float sc = n < p.rows ? __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale : 0.f;
+    const int cols_half = p.Np / 2;
+    for (int c0 = half * cols_half; c0 < (half + 1) * cols_half; c0 += 16) {
+      uint32_t v[16];
+      tc_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0), v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int m = c0 + j;
+        if (m < p.M && n < p.rows) {
+          p.y[static_cast<long long>(m) * p.ldy + n] =
+              __half_as_ushort(__float2half_rn(__uint_as_float(v[j]) * sc));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kTcDecodeWarps) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(geo.tmem_cols));
+  }
+}
+
+}  // namespace dev
+
+// ---------------------------------------------------------------- launchers
+template <int SCHEME>
+static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long long ldx,
+                               long long cols, cudaStream_t s) {
+  using T = dev::Traits<SCHEME>;
+  // activation prep (PDL-chained)
+  {
+    const long long total = static_cast<long long>(p.k_tiles) * T::kTK * p.Np;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(total / 256 + 1 < 148 * 16 ? total / 256 + 1 : 148 * 16));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_xprep_tc_kernel<SCHEME>, x, ldx, cols, p.M,
+                                       p.Np, p.k_tiles, const_cast<unsigned short*>(p.xk));
+    count_launch();
+    if (e != cudaSuccess) return e;
+  }
+  dev::TcGeom geo{};
+  const int budget = 220 * 1024;
+  for (int kc : {4, 2, 1}) {
+    geo.kchunk = kc;
+    geo.a_bytes = 128 * kc * T::kTK * 2;
+    geo.b_bytes = p.Np * kc * T::kTK * 2;
+    geo.stage = (geo.a_bytes + geo.b_bytes + 1023) / 1024 * 1024;
+    geo.stages = budget / geo.stage;
+    if (geo.stages >= 3) break;
+  }
+  if (geo.stages > 6) geo.stages = 6;
+  if (geo.stages < 2) return cudaErrorInvalidConfiguration;
+  geo.tmem_cols = 32;
+  while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
+  const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((p.row_tiles + 7) / 8));
+  cfg.blockDim = dim3(dev::kTcThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME>, p, geo);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
+                             long long cols, cudaStream_t s) {
+  if (p.row_tiles <= 0) return cudaSuccess;
+  return p.scheme_id == 4 ? launch_tc_t<4>(p, x, ldx, cols, s) : launch_tc_t<7>(p, x, ldx, cols, s);
+}
+
+}  // namespace amsqb

@@ -66,14 +66,28 @@ def decode_s7(R: np.ndarray) -> np.ndarray:
     return A
 
 
-def placed_matrix(scheme: int, tiles: np.ndarray, row_tiles: int, k_tiles: int) -> np.ndarray:
+def tile_offsets(plan, row_tiles: int, k_tiles: int) -> np.ndarray:
+    """[row_tiles][k_tiles] storage index of each tile: groups of g_big (the first n_big)
+    or g_big - 1 row tiles, stored [group][k_tile][row_tile_in_group] (device_layout.hpp)."""
+    n_groups, g_big, n_big, _ = plan
+    off = np.zeros((row_tiles, k_tiles), np.int64)
+    r0 = 0
+    for g in range(n_groups):
+        G = g_big if g < n_big else g_big - 1
+        for r in range(G):
+            off[r0 + r] = r0 * k_tiles + np.arange(k_tiles) * G + r
+        r0 += G
+    assert r0 == row_tiles
+    return off
+
+
+def placed_matrix(scheme: int, tiles: np.ndarray, row_tiles: int, k_tiles: int,
+                  plan) -> np.ndarray:
     """Dense [row_tiles*16][k_tiles*TK] matrix of the placed binary16 bits the MMAs see,
     with every A-fragment element put at the column its B-fragment partner selects."""
     tr = TRAITS[scheme]
     tb, TK, J, LK = tr["tile_bytes"], tr["tk"], tr["J"], tr["lane_k"]
-    # storage order [row_block][k_tile][row_tile_in_block] (device_layout.hpp)
-    t = tiles.reshape(row_tiles // 16, k_tiles, 16, tb).transpose(0, 2, 1, 3).reshape(
-        row_tiles, k_tiles, tb)
+    t = tiles.reshape(-1, tb)[tile_offsets(plan, row_tiles, k_tiles)]
     R = t[:, :, :512].copy().view(np.uint32).reshape(row_tiles, k_tiles, 32, 4)
     if scheme == 4:
         A = decode_s4(R, t[:, :, 512:544].astype(U32))

@@ -184,3 +184,19 @@ def test_cpp_dropin_against_reference(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "0 failure(s)" in r.stdout
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("shape", [(128, 64), (300, 1000), (1000, 4098)])
+@pytest.mark.parametrize("batch", [24, 32, 64, 100, 256, 300])
+def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch):
+    """M > 16 runs K3 (tcgen05.mma + TMEM, up to 256 batch rows per launch)."""
+    rows, cols = shape
+    qt = quantized_gaussian(sid, rows, cols, seed=batch * 3 + rows)
+    x = gaussian_x(batch, cols, seed=batch + 11)
+    dw = amsq.DeviceWeight(qt)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = dw.linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)

@@ -208,6 +208,33 @@ def _repack(qt):
     return tiles, back
 
 
+def _plan(sid, rows, cols):
+    plan = (C.c_int * 4)()
+    from paper_2510_16045_b200._lib import check
+    check(lib().amsq_device_layout_plan(sid, rows, cols, plan), "plan")
+    return tuple(plan)
+
+
+@pytest.mark.parametrize("sid", [4, 7])
+def test_work_plans_at_config_shapes(sid):
+    """Every Llama-3.1-8B/70B (and TP-shard) shape gets a plan that covers its row tiles
+    exactly, fits 148 SMs, keeps <= 64 row tiles per CTA and balances within 16 %."""
+    shapes = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336), (10240, 8192),
+              (8192, 8192), (57344, 8192), (8192, 28672), (1280, 8192), (1024, 8192),
+              (7168, 8192), (1024, 28672), (33, 200), (1, 3)]
+    tk = 64 if sid == 4 else 48
+    for rows, cols in shapes:
+        n_groups, g_big, n_big, cs = _plan(sid, rows, cols)
+        rt = -(-rows // 16)
+        kt = -(-amsq.round_up(cols, amsq.scheme_by_id(sid).block) // tk)
+        assert n_big * g_big + (n_groups - n_big) * (g_big - 1) == rt
+        assert 1 <= n_big <= n_groups and n_groups * cs <= 148 and 1 <= g_big <= 64
+        assert cs in (1, 2, 4, 8)
+        if rt * kt >= 148 * 32:  # big enough to fill the GPU: per-CTA work near the ideal
+            ideal = rt * kt / 148
+            assert g_big * -(-kt // cs) <= 1.16 * ideal + g_big, (rows, cols, n_groups, g_big, cs)
+
+
 LAYOUT_SHAPES = [(1, 3), (1, 64), (16, 48), (33, 200), (40, 100), (257, 4096), (300, 4098),
                  (17, 14336)]
 
@@ -236,9 +263,9 @@ def test_emulated_kernel_decode_restores_reference_grid(orc, sid, shape):
         qt = amsq.quantize_tensor(np.random.default_rng(1).standard_normal((rows, cols)).astype(np.float32), sid)
     tiles, _ = _repack(qt)
     tk = emulate.TRAITS[sid]["tk"]
-    row_tiles = -(-rows // 256) * 16
+    row_tiles = -(-rows // 16)
     k_tiles = -(-qt.padded_cols // tk)
-    placed = emulate.placed_matrix(sid, tiles, row_tiles, k_tiles)
+    placed = emulate.placed_matrix(sid, tiles, row_tiles, k_tiles, _plan(sid, rows, cols))
     grid = emulate.placed_to_grid(placed)[:rows, :qt.padded_cols]
     want = orc.restore_grid(sid, rows, qt.padded_cols, qt.payload)
     # -0 codes place to 0x8000 and stay -0 after the exact rescale

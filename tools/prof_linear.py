@@ -27,13 +27,9 @@ def main():
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--cublas", action="store_true")
     ap.add_argument("--graph", action="store_true")
-    ap.add_argument("--dry", type=int, default=0,
-                    help="1: consumers skip decode/MMA, 2: skip MMA, 3: skip decode")
     ap.add_argument("--empty", action="store_true", help="time an empty kernel per call")
     args = ap.parse_args()
     sid = amsq.scheme_by_name(args.scheme).id
-    from paper_2510_16045_b200._lib import lib
-    lib().amsq_debug_set_dry_run(args.dry)
     copies = max(2, int(np.ceil(260e6 / amsq.packed_payload_bytes(sid, args.n, args.k))))
     ws = [amsq.DeviceWeight(bench.make_payload(sid, args.n, args.k, seed=c)) for c in range(copies)]
     x = torch.randn(args.m, args.k, device="cuda").half()
@@ -62,7 +58,7 @@ def main():
             torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / (200 * reps)
         pb = ws[0].payload_bytes
-        print(f"graph dry={args.dry}: {args.scheme} N={args.n} K={args.k} M={args.m}: {us:.2f} us/call, "
+        print(f"graph: {args.scheme} N={args.n} K={args.k} M={args.m}: {us:.2f} us/call, "
               f"{pb / us / 1e3:.0f} GB/s packed  clocks={clk.summary()}")
 
 

@@ -10,29 +10,34 @@ from paper_2510_16045_b200._lib import lib  # noqa
 ap = argparse.ArgumentParser()
 ap.add_argument("--scheme", default="fp5.33-e2m3"); ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--k", type=int, default=4096); ap.add_argument("--m", type=int, default=1)
-ap.add_argument("--dry", action="store_true")
 a = ap.parse_args()
 sid = amsq.scheme_by_name(a.scheme).id
-lib().amsq_debug_set_dry_run(1 if a.dry else 0)
 ws = [amsq.DeviceWeight(bench.make_payload(sid, a.n, a.k, seed=c)) for c in range(3)]
 x = torch.randn(a.m, a.k, device="cuda").half(); y = torch.empty(a.m, a.n, device="cuda", dtype=torch.float16)
-tr = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(1024 * 64, dtype=torch.int64, device="cuda")
 for i in range(6): ws[i % 3].linear(x, out=y)
 torch.cuda.synchronize()
 lib().amsq_debug_set_trace(tr.data_ptr())
 ws[0].linear(x, out=y); torch.cuda.synchronize()
 lib().amsq_debug_set_trace(None)
-t = tr.view(1024, 8).cpu().numpy().astype(np.float64)
+info = ws[0].info()
+t = tr.view(1024, 64).cpu().numpy().astype(np.float64)
 nct = int((t[:, 0] > 0).sum())
 t = t[:nct]
 t0 = t[:, 0].min()
-st, first, loop, end = [(t[:, i] - t0) / 1e3 for i in range(4)]
+rel = lambda v: (v - t0) / 1e3
+st, first, loop, end = [rel(t[:, i]) for i in range(4)]
 def q(v): return f"min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}"
-print(f"{a.scheme} N={a.n} K={a.k} M={a.m} dry={a.dry} ctas={len(t)} (us from first CTA start)")
+print(f"{a.scheme} N={a.n} K={a.k} M={a.m} ctas={len(t)} plan=(groups {info.n_groups}, G {info.g_big}, "
+      f"big {info.n_big}, csplit {info.csplit}) (us from first CTA start)")
 print("  start      ", q(st)); print("  first stage", q(first)); print("  stream done", q(loop)); print("  end        ", q(end))
-print("  first-stage latency per CTA", q(first - st), " fixup per CTA", q(end - loop))
-
-slots = np.arange(len(t)) // 148
-for sl in range(slots.max() + 1):
-    sel = slots == sl
-    print(f"  CTA slot {sl} (blockIdx {sl*148}..): stream done", q(loop[sel]), " end", q(end[sel]))
+print("  first-stage latency per CTA", q(first - st), " epilogue per CTA", q(end - loop))
+GHZ = 1.9  # SM clock under this load (clocks.sm ~1965 MHz); stamps 4.. are clock64
+clk = lambda c, v: st[c] + (v - t[c, 63]) / GHZ / 1e3
+print("  producer stamps (CTA 0): after pdl_wait + x issues:",
+      " ".join(f"{clk(0, t[0, 4 + i]):.2f}" for i in range(4) if t[0, 4 + i] > 0))
+for c in (0, len(t) // 2):
+    land = [clk(c, t[c, 8 + 2 * s]) for s in range(28) if t[c, 8 + 2 * s] > 0]
+    done = [clk(c, t[c, 9 + 2 * s]) for s in range(28) if t[c, 9 + 2 * s] > 0]
+    print(f"  CTA {c}: start {st[c]:.2f}; stage landed/consumed:",
+          " ".join(f"{l:.2f}/{d:.2f}" for l, d in zip(land, done)))
