@@ -281,6 +281,22 @@ def run_ours(args, world, rank, local):
 
     # --- end to end through the C-ABI with pinned host buffers
     e2e = run_e2e(args, sets, shapes, calls, payload_bytes, dev, world)
+    extra = {}
+    if not args.no_extra and rank == 0:
+        for c in sets:
+            for w in c.values():
+                w.free()
+        torch.cuda.empty_cache()
+        t = time.time()
+        for key, fn in (("batch_sweep", lambda: run_batch_sweep(args, shapes, dev, stream, cap)),
+                        ("stack_32L", lambda: run_stack(args, shapes, dev, stream, cap)),
+                        ("tp_shards_70B", lambda: run_tp_shards(args, dev, stream, cap))):
+            try:
+                extra[key] = fn()
+            except Exception as e:  # an extra section must not take the headline line down
+                torch.cuda.synchronize()
+                extra[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        extra["extra_seconds"] = round(time.time() - t, 1)
 
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -315,9 +331,181 @@ def run_ours(args, world, rank, local):
         "clocks": clk.summary(),
         "detail": detail,
     }
+    line.update(extra)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, shapes, batches, sid, sample_only=True)
     return line
+
+
+def _graph_us(fn, reps_in_graph, replays, stream, cap):
+    """Device time per call of `fn(r)` captured reps_in_graph times in one CUDA graph."""
+    import torch
+    with torch.cuda.stream(cap):
+        fn(0)
+        cap.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            for r in range(reps_in_graph):
+                fn(r)
+    stream.wait_stream(cap)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(replays):
+        g.replay()
+    b.record(stream)
+    torch.cuda.synchronize()
+    del g
+    return a.elapsed_time(b) * 1e3 / (replays * reps_in_graph)
+
+
+def _rotation(w, min_bytes=260e6):
+    """w plus device clones so a rotation over them streams > 2x the 126 MB L2."""
+    n = max(2, int(np.ceil(min_bytes / w.payload_bytes)))
+    return [w] + [w.clone() for _ in range(n - 1)]
+
+
+def run_batch_sweep(args, shapes, dev, stream, cap):
+    """Config 3: both schemes x 8B shapes x M in 1..256 (memory-bound -> tcgen05 crossover)."""
+    import torch
+    import torch.nn.functional as F
+
+    import paper_2510_16045_b200 as amsq
+    from paper_2510_16045_b200._lib import lib
+    batches = [int(b) for b in args.sweep_batches.split(",")]
+    peak, tpeak, _ = _peaks()
+    out = []
+    dense = {name: [torch.randn(n, k, device=dev).half() for _ in range(2)]
+             for name, (n, k) in shapes.items()}
+    cub = {}
+    for name, (n, k) in shapes.items():
+        for m in batches:
+            x = torch.randn(m, k, device=dev).half()
+            cub[(name, m)] = _graph_us(lambda r, x=x, name=name: F.linear(x, dense[name][r % 2]),
+                                       8, 5, stream, cap)
+    del dense
+    torch.cuda.empty_cache()
+    for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
+        sid = amsq.scheme_by_name(scheme).id
+        for i, (name, (n, k)) in enumerate(shapes.items()):
+            ws = _rotation(amsq.DeviceWeight(make_payload(sid, n, k, seed=500 + i), device=dev.index))
+            pb = ws[0].payload_bytes
+            for m in batches:
+                x = torch.randn(m, k, device=dev).half()
+                y = torch.empty(m, n, device=dev, dtype=torch.float16)
+
+                def call(r, x=x, y=y, m=m):
+                    rc = lib().amsq_linear(ws[r % len(ws)].handle, x.data_ptr(), m, y.data_ptr(),
+                                           cap.cuda_stream)
+                    if rc:
+                        raise RuntimeError(lib().amsq_last_error().decode())
+                us = _graph_us(call, 2 * len(ws), 5, stream, cap)
+                flops = 2.0 * m * n * k
+                out.append({"scheme": scheme, "layer": name, "N": n, "K": k, "M": m,
+                            "kernel": "K2 mma.sync" if m <= 16 else "K3 tcgen05",
+                            "us": round(us, 2), "packed_GBps": round(pb / us / 1e3, 1),
+                            "hbm_frac": round(algorithmic_bytes(pb, n, k, m) / us / 1e3 / peak, 3),
+                            "TFLOPs": round(flops / us / 1e6, 1),
+                            "tensor_frac": round(flops / us / 1e6 / tpeak, 3),
+                            "cublas_fp16_us": round(cub[(name, m)], 2),
+                            "speedup_vs_cublas": round(cub[(name, m)] / us, 2)})
+            for w in ws:
+                w.free()
+    return out
+
+
+def run_stack(args, shapes, dev, stream, cap):
+    """Config 5: the 32-layer Llama-3.1-8B decode-step linear stack (qkv, o, gate_up, down per
+    layer = 128 linears, distinct weights in HBM) as ONE CUDA graph, FP5.33 vs FP4.25 vs FP16
+    cuBLAS, per batch."""
+    import torch
+    import torch.nn.functional as F
+
+    import paper_2510_16045_b200 as amsq
+    from paper_2510_16045_b200._lib import lib
+    batches = [int(b) for b in args.stack_batches.split(",")]
+    L = args.stack_layers
+    res = {"layers": L, "linears": 4 * L, "batches": batches}
+    xs = {m: {name: torch.randn(m, k, device=dev).half() for name, (n, k) in shapes.items()}
+          for m in batches}
+    ys = {m: {name: torch.empty(m, n, device=dev, dtype=torch.float16)
+              for name, (n, k) in shapes.items()} for m in batches}
+    for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
+        sid = amsq.scheme_by_name(scheme).id
+        base = {name: amsq.DeviceWeight(make_payload(sid, n, k, seed=900 + i), device=dev.index)
+                for i, (name, (n, k)) in enumerate(shapes.items())}
+        layers = [base] + [{name: w.clone() for name, w in base.items()} for _ in range(L - 1)]
+        total_bytes = sum(w.payload_bytes for lay in layers for w in lay.values())
+        per = {}
+        for m in batches:
+            def step(r, m=m):
+                for lay in layers:
+                    for name in shapes:
+                        rc = lib().amsq_linear(lay[name].handle, xs[m][name].data_ptr(), m,
+                                               ys[m][name].data_ptr(), cap.cuda_stream)
+                        if rc:
+                            raise RuntimeError(lib().amsq_last_error().decode())
+            us = _graph_us(step, 1, 5, stream, cap)
+            per[str(m)] = {"us": round(us, 1), "packed_GBps": round(total_bytes / us / 1e3, 1)}
+        res[scheme] = {"weight_bytes": total_bytes, "per_batch": per}
+        for lay in layers:
+            for w in lay.values():
+                w.free()
+        torch.cuda.empty_cache()
+    dense = [{name: torch.randn(n, k, device=dev).half() for name, (n, k) in shapes.items()}
+             for _ in range(L)]
+    per = {}
+    for m in batches:
+        def step16(r, m=m):
+            for lay in dense:
+                for name in shapes:
+                    F.linear(xs[m][name], lay[name], out=None)
+        us = _graph_us(step16, 1, 5, stream, cap)
+        per[str(m)] = {"us": round(us, 1)}
+    res["fp16-cublas"] = {"weight_bytes": sum(2 * n * k for n, k in shapes.values()) * L,
+                          "per_batch": per}
+    for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
+        for m in batches:
+            res[scheme]["per_batch"][str(m)]["speedup_vs_cublas"] = round(
+                per[str(m)]["us"] / res[scheme]["per_batch"][str(m)]["us"], 2)
+    del dense
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_tp_shards(args, dev, stream, cap):
+    """Config 4 on one GPU: the per-rank share of the N-sharded Llama-3.1-70B linears at
+    P = 2/4/8 (rows N/P, full K). The NCCL all-gather itself needs P GPUs (not timed here)."""
+    import torch
+
+    import paper_2510_16045_b200 as amsq
+    from paper_2510_16045_b200._lib import lib
+    out = []
+    for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
+        sid = amsq.scheme_by_name(scheme).id
+        for i, (name, (n, k)) in enumerate(SHAPES_70B.items()):
+            for P in (2, 4, 8):
+                rows = n // P
+                ws = _rotation(amsq.DeviceWeight(make_payload(sid, rows, k, seed=700 + i), device=dev.index))
+                pb = ws[0].payload_bytes
+                for m in (1, 16):
+                    x = torch.randn(m, k, device=dev).half()
+                    y = torch.empty(m, rows, device=dev, dtype=torch.float16)
+
+                    def call(r, x=x, y=y, m=m):
+                        rc = lib().amsq_linear(ws[r % len(ws)].handle, x.data_ptr(), m,
+                                               y.data_ptr(), cap.cuda_stream)
+                        if rc:
+                            raise RuntimeError(lib().amsq_last_error().decode())
+                    us = _graph_us(call, 2 * len(ws), 5, stream, cap)
+                    out.append({"scheme": scheme, "layer": name, "P": P, "rows_per_rank": rows,
+                                "K": k, "M": m, "us": round(us, 2),
+                                "packed_GBps_per_rank": round(pb / us / 1e3, 1),
+                                "allgather_bytes_per_rank": 2 * m * n * (P - 1) // P})
+                for w in ws:
+                    w.free()
+    return out
 
 
 def run_e2e(args, sets, shapes, calls, payload_bytes, dev, world):
@@ -465,6 +653,11 @@ def main():
     ap.add_argument("--batches", default="1,4,8,16")
     ap.add_argument("--copies", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the batch sweep (config 3), 32-layer stack (config 5), TP shards")
+    ap.add_argument("--sweep-batches", default="1,2,4,8,16,32,64,128,256")
+    ap.add_argument("--stack-batches", default="1,4,8,16")
+    ap.add_argument("--stack-layers", type=int, default=32)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = _dist()

@@ -126,6 +126,9 @@ int amsq_weight_upload_container(const uint8_t* in, size_t in_bytes, size_t row0
                                  int device, void* stream, amsq_weight_t* out);
 int amsq_weight_download(amsq_weight_t h, uint16_t* scales, size_t n_scales, uint16_t* payload,
                          size_t payload_words);
+/* A second, independent device copy of h (same device; a device-to-device copy of the tile
+ * layout -- e.g. to lay out many layers of identical shape without re-uploading). */
+int amsq_weight_clone(amsq_weight_t h, void* stream, amsq_weight_t* out);
 int amsq_weight_free(amsq_weight_t h);
 
 typedef struct {

@@ -10,6 +10,8 @@ import ctypes as C
 import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libamsq_b200.so")
+# experiments only (tools/): load a variant build of the same library, e.g. build/variants/*.so
+LIB_PATH = os.environ.get("AMSQ_LIB", LIB_PATH)
 
 AMSQ_OK, AMSQ_EINVAL, AMSQ_ECORRUPT, AMSQ_ECUDA, AMSQ_ENCCL, AMSQ_ENOMEM, AMSQ_ENODEV = range(7)
 
@@ -76,6 +78,7 @@ SIGNATURES = {
                                      C.POINTER(_P)]),
     "amsq_weight_upload_container": (_I, [_U8P, _SZ, _SZ, _SZ, _I, _P, C.POINTER(_P)]),
     "amsq_weight_download": (_I, [_P, _U16P, _SZ, _U16P, _SZ]),
+    "amsq_weight_clone": (_I, [_P, _P, C.POINTER(_P)]),
     "amsq_weight_free": (_I, [_P]),
     "amsq_weight_info": (_I, [_P, C.POINTER(WeightInfo)]),
     "amsq_restore_grid_f16": (_I, [_P, _P, _P]),

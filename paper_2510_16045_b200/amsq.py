@@ -340,6 +340,16 @@ class DeviceWeight:
               "gemv")
         return y
 
+    def clone(self, stream=None) -> "DeviceWeight":
+        """An independent device copy (device-to-device; no host round trip)."""
+        out = DeviceWeight.__new__(DeviceWeight)
+        out._h = C.c_void_p(None)
+        check(lib().amsq_weight_clone(self._h, _stream_ptr(stream), C.byref(out._h)), "clone")
+        for k in ("scheme", "rows", "cols", "padded_cols", "device", "device_bytes", "payload_bytes"):
+            if hasattr(self, k):
+                setattr(out, k, getattr(self, k))
+        return out
+
     def free(self):
         if self._h and self._h.value:
             lib().amsq_weight_free(self._h)

@@ -24,7 +24,6 @@ struct amsq_weight_s {
   uint8_t* d_w = nullptr;
   unsigned short* d_scales = nullptr;
   uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 16 batch rows)
-  unsigned short* d_xk = nullptr;  // K3 activation image (<= 256 batch rows), lazily allocated
 };
 
 namespace {
@@ -87,6 +86,13 @@ void require_device(int device) {
   if (device < 0 || device >= n) throw amsqb::InvalidArgument("device index out of range");
   cudaDeviceProp prop{};
   ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  // keep the stream-ordered pool's memory cached (the per-call scratch of amsq_gemv_host and
+  // K3 would otherwise be unmapped and re-mapped on every synchronising call)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (prop.major != 10) {
     throw NoDevice("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
                    "; this library is built for sm_100a (B200) only");
@@ -151,7 +157,6 @@ void free_impl(amsq_weight_t h) {
   cudaFree(h->d_w);
   cudaFree(h->d_scales);
   cudaFree(h->d_xperm);
-  cudaFree(h->d_xk);
   delete h;
 }
 
@@ -177,15 +182,17 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.trace = g_trace;
   if (batch > static_cast<size_t>(amsqb::linear_max_batch_per_launch())) {
     // K3: tcgen05 tiles, up to 256 batch rows per launch (weights streamed once per launch)
-    if (!h->d_xk) {
-      ck(cudaMalloc(&h->d_xk, static_cast<size_t>(amsqb::kTcMaxBatch) * h->L.k_tiles * h->L.tk * 2),
-         "cudaMalloc(xk)");
-    }
+    // the activation image is stream-ordered scratch (cudaMallocAsync: capturable in CUDA
+    // graphs, pooled, and private to this call -- no race between streams)
+    void* xk = nullptr;
+    const size_t mb_max = batch < static_cast<size_t>(amsqb::kTcMaxBatch) ? batch : amsqb::kTcMaxBatch;
+    ck(cudaMallocAsync(&xk, (mb_max + 15) / 16 * 16 * h->L.k_tiles * h->L.tk * 2, st),
+       "cudaMallocAsync(xk)");
     amsqb::TcParams q{};
     q.scheme_id = h->L.scheme_id;
     q.w = h->d_w;
     q.scales = h->d_scales;
-    q.xk = h->d_xk;
+    q.xk = static_cast<const unsigned short*>(xk);
     q.rows = p.rows;
     q.ldy = p.ldy;
     q.row_tiles = p.row_tiles;
@@ -200,6 +207,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
                                  p.cols, p.cols, st),
          "amsq_linear_tc_kernel launch");
     }
+    ck(cudaFreeAsync(xk, st), "cudaFreeAsync(xk)");
     return;
   }
   const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
@@ -427,6 +435,26 @@ int amsq_weight_download(amsq_weight_t h, uint16_t* scales, size_t n_scales, uin
       ck(cudaMemcpy(tiles.data(), h->d_w, tiles.size(), cudaMemcpyDeviceToHost), "D2H weights");
       amsqb::repack_from_device(L, tiles.data(), payload, 0);
     }
+  });
+}
+
+int amsq_weight_clone(amsq_weight_t h, void* stream, amsq_weight_t* out) {
+  return guarded([&] {
+    check_handle(h);
+    if (!out) throw amsqb::InvalidArgument("null output handle");
+    DeviceGuard dg(h->device);
+    auto c = std::make_unique<amsq_weight_s>();
+    c->device = h->device;
+    c->L = h->L;
+    cudaStream_t st = as_stream(stream);
+    ck(cudaMalloc(&c->d_w, h->L.bytes()), "cudaMalloc(weights)");
+    ck(cudaMalloc(&c->d_scales, h->L.row_tiles * 16 * sizeof(unsigned short)), "cudaMalloc(scales)");
+    ck(cudaMalloc(&c->d_xperm, h->L.k_tiles * 4 * 16 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
+    ck(cudaMemcpyAsync(c->d_w, h->d_w, h->L.bytes(), cudaMemcpyDeviceToDevice, st), "D2D weights");
+    ck(cudaMemcpyAsync(c->d_scales, h->d_scales, h->L.row_tiles * 16 * 2, cudaMemcpyDeviceToDevice, st),
+       "D2D scales");
+    ck(cudaStreamSynchronize(st), "clone sync");
+    *out = c.release();
   });
 }
 

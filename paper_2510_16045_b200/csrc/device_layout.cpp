@@ -46,9 +46,10 @@ void choose_plan(size_t RT, size_t KT, DeviceLayout* L) {
     for (size_t ng = 1; ng <= max_groups; ++ng) {
       const size_t G = (RT + ng - 1) / ng;
       if (G > static_cast<size_t>(kMaxGroupTiles) || (RT + G - 1) / G != ng) continue;
-      // a cluster's DSMEM reduction costs about one k-tile of streaming per rank
-      const double work = static_cast<double>(G) *
-                          (static_cast<double>((KT + C - 1) / C) + (C > 1 ? 0.5 * C : 0.0));
+      // a cluster's DSMEM reduction (remote stores of G row tiles' partials + one cluster
+      // barrier) costs about one k-tile per row tile plus ~3 k-tiles of barrier latency
+      const double work = static_cast<double>(G) * static_cast<double>((KT + C - 1) / C) +
+                          (C > 1 ? static_cast<double>(G) + 3.0 : 0.0);
       cands.push_back({work, static_cast<int>(ng) * C, C, static_cast<int>(ng),
                        static_cast<int>(G)});
     }

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <type_traits>
 #include <cstdint>
 
 #include "kernels.h"
@@ -166,7 +167,13 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 //    CTAs of a cluster are summed in rank order through DSMEM, scale * 2^14, fp16 round.
 //    Deterministic: the summation order depends only on the shape.
 // =====================================================================================
-constexpr int kConsumerWarps = 16;
+#ifndef AMSQ_K2_WARPS
+#define AMSQ_K2_WARPS 16
+#endif
+#ifndef AMSQ_K2_MODE  // profiling variants only (tools/build_variants.sh): 1 = stream only,
+#define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode
+#endif
+constexpr int kConsumerWarps = AMSQ_K2_WARPS;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
 constexpr int kMaxOwn = 4;                              // row tiles per consumer warp
 
@@ -188,13 +195,6 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
-}
-__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
-  return v;
 }
 
 template <int SCHEME, int NB>
@@ -376,73 +376,91 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
     };
     // weights of the first ring-full of stages are independent of the previous kernel:
     // request them before griddepcontrol.wait
-    const int first = min(nst, geo.stages);
-    if (lane == 0) {
-      for (int st = 0; st < first; ++st) issue_w(st, st);
-    }
+    // stage 0's weights do not depend on the previous kernel: request them before
+    // griddepcontrol.wait. Later stages go weights-then-activations, so the TMA queue never
+    // holds a ring's worth of weights in front of the activations the first stage needs.
+    if (lane == 0 && nst > 0) issue_w(0, 0);
     pdl_wait();  // activations may be produced by the previous kernel
     if (trace && lane == 0) trace[4] = clock64();
     int sidx = 0;
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
-      if (st >= geo.stages) {
-        mbar_wait(&empty[sidx], ph ^ 1u);
+      if (st > 0) {
+        if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
         if (lane == 0) issue_w(st, sidx);
       }
       issue_x(st, sidx);
-      if (trace && lane == 0 && st < 3) trace[5 + st] = clock64();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
   } else {
     // ------------------------------------------------------------------ consumers
+    // the warp's kpw k-tiles x NOWN row tiles of a stage, branch-free for a fixed NOWN
+    auto consume = [&](const uint8_t* sp, int nk, auto nown_c) {
+      constexpr int NOWN = decltype(nown_c)::value;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int kq = geo.kpw * ks + kk;
+        if (kk < geo.kpw && kq < nk) {
+          uint32_t B[NB][J][2];
+          load_bfrag<SCHEME, NB>(sp + geo.w_stage, geo, kq, g, t, B);
+          const uint8_t* tb = sp + (kq * G + rl) * TILE + lane * 16;
+          uint4 wv[NOWN];
+          uint32_t sh[NOWN];
+#pragma unroll
+          for (int i = 0; i < NOWN; ++i) {
+            const uint8_t* tp = tb + i * geo.wr * TILE;
+            wv[i] = *reinterpret_cast<const uint4*>(tp);
+            sh[i] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
+          }
+#pragma unroll
+          for (int i = 0; i < NOWN; ++i) {
+            uint32_t A[J][4];
+            const uint32_t R[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
+#if AMSQ_K2_MODE == 3  // profiling variant: MMA on masked raw words (no decode)
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) A[j][q] = R[(j + q) & 3] & 0x3F003F00u;
+#else
+            if constexpr (SCHEME == 4) {
+              decode_s4(R, sh[i], A);
+            } else {
+              decode_s7(R, A);
+            }
+#endif
+#if AMSQ_K2_MODE == 2  // profiling variant: decode without the tensor cores
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+              acc[i][0][j & 3] += __uint_as_float((A[j][0] ^ A[j][1] ^ A[j][2] ^ A[j][3] ^ B[0][j][0]) & 0x3F0F0F0Fu);
+#else
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int j = 0; j < J; ++j) mma16816(acc[i][nb], A[j], B[nb][j][0], B[nb][j][1]);
+#endif
+          }
+        }
+      }
+    };
     int sidx = 0;
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
       mbar_wait(&full[sidx], ph);
-      if (trace && threadIdx.x == 0) {
-        if (st == 0) trace[1] = globaltimer();
-        if (st < 28) trace[8 + 2 * st] = clock64();
-      }
+      if (trace && st == 0 && threadIdx.x == 0) trace[1] = globaltimer();
       const int nk = min(S, L - st * S);
       const uint8_t* sp = smem + sidx * geo.stage;
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {  // the warp's k-tiles of the stage (kpw = 1 or 2)
-        const int kq = geo.kpw * ks + kk;
-        if (kk < geo.kpw && kq < nk && nown > 0) {
-          uint32_t B[NB][J][2];
-          load_bfrag<SCHEME, NB>(sp + geo.w_stage, geo, kq, g, t, B);
-          const uint8_t* tb = sp + (kq * G + rl) * TILE + lane * 16;
-          uint4 wv[kMaxOwn];
-          uint32_t sh[kMaxOwn];
-#pragma unroll
-          for (int i = 0; i < kMaxOwn; ++i) {
-            if (i < nown) {
-              const uint8_t* tp = tb + i * geo.wr * TILE;
-              wv[i] = *reinterpret_cast<const uint4*>(tp);
-              sh[i] = SCHEME == 4 ? tp[512 - lane * 16 + lane] : 0u;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < kMaxOwn; ++i) {
-            if (i < nown) {
-              uint32_t A[J][4];
-              const uint32_t R[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
-              if constexpr (SCHEME == 4) {
-                decode_s4(R, sh[i], A);
-              } else {
-                decode_s7(R, A);
-              }
-#pragma unroll
-              for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                for (int j = 0; j < J; ++j) mma16816(acc[i][nb], A[j], B[nb][j][0], B[nb][j][1]);
-            }
-          }
-        }
+#if AMSQ_K2_MODE == 1
+      if (false)
+#endif
+      switch (nown) {  // warp-uniform and fixed per warp
+        case 1: consume(sp, nk, std::integral_constant<int, 1>{}); break;
+        case 2: consume(sp, nk, std::integral_constant<int, 2>{}); break;
+        case 3: consume(sp, nk, std::integral_constant<int, 3>{}); break;
+        case 4: consume(sp, nk, std::integral_constant<int, 4>{}); break;
+        default: break;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sidx]);
-      if (trace && threadIdx.x == 0 && st < 28) trace[9 + 2 * st] = clock64();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
     if (trace && threadIdx.x == 0) trace[2] = globaltimer();
@@ -467,7 +485,10 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
   }
   __syncthreads();
   pdl_wait();  // outputs may still be read by the previous kernel
-  float* part = red + static_cast<long long>(nslots) * items;  // [G][32][NB4] (clusters)
+  // clusters: recv[C][items] -- rank q's partial of the items rank r finalises lands in
+  // rank r's recv[q] (remote stores), one cluster barrier, then rank r sums in rank order
+  float* recv = red + static_cast<long long>(nslots) * items;
+  const int Gs = (G + CS - 1) / CS;  // row tiles each rank finalises
   auto store_y = [&](int it, float v) {
     const int r = it / (32 * NB4), rem = it - r * 32 * NB4;
     const int ln = rem / NB4, q = rem - ln * NB4, nb = q >> 2, e = q & 3;
@@ -484,22 +505,27 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
     if constexpr (CS == 1) {
       store_y(it, v);
     } else {
-      part[it] = v;
+      const uint32_t owner = static_cast<uint32_t>((it / (32 * NB4)) / Gs);
+      float* dst = recv + static_cast<long long>(crank) * items + it;
+      if (owner == crank) {
+        *dst = v;
+      } else {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(dst)), "r"(owner));
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+      }
     }
   }
   if constexpr (CS > 1) {
-    cluster_sync_all();  // every CTA's partial visible cluster-wide
-    // rank r finalises row tiles [r*Gs, (r+1)*Gs), summing the CS partials in rank order
-    const int Gs = (G + CS - 1) / CS;
+    cluster_sync_all();  // every rank's partials have landed in their owners' recv
     const int i0 = min(G, static_cast<int>(crank) * Gs) * 32 * NB4;
     const int i1 = min(G, static_cast<int>(crank + 1) * Gs) * 32 * NB4;
     for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
       float v = 0.0f;
 #pragma unroll
-      for (int r = 0; r < CS; ++r) v += ld_dsmem_f32(part + it, static_cast<uint32_t>(r));
+      for (int r = 0; r < CS; ++r) v += recv[static_cast<long long>(r) * items + it];  // rank order
       store_y(it, v);
     }
-    cluster_sync_all();  // keep our shared memory alive until every peer has read it
   }
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
 }
@@ -539,8 +565,15 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   using T = dev::Traits<SCHEME>;
   dev::K2Geom geo{};
   const int G = p.plan.g_big;
-  int wr = 1;
-  while (wr < 16 && (G + wr - 1) / wr > 2) wr *= 2;
+  // wr: the smallest divisor of the consumer-warp count giving each warp <= 2 row tiles
+  // (<= 4 when even all warps on one k-slot cannot)
+  int wr = dev::kConsumerWarps;
+  for (int d = 1; d <= dev::kConsumerWarps; ++d) {
+    if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= 2) {
+      wr = d;
+      break;
+    }
+  }
   geo.wr = wr;
   geo.kpw = NB == 2 ? 1 : 2;  // M <= 16 carries 2x the activation bytes per k-tile
   geo.S = geo.kpw * (dev::kConsumerWarps / wr);
@@ -554,8 +587,8 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const int budget = 227 * 1024 - 1024;
   geo.stages = budget / geo.stage;
   if (geo.stages > 6) geo.stages = 6;
-  // the epilogue reuses the ring: (S/kpw + 1) x G x 32 x NB*4 floats
-  const long long red = (static_cast<long long>(geo.S / geo.kpw) + 1) * G * 32 * NB * 4 * 4;
+  // the epilogue reuses the ring: (S/kpw + csplit) x G x 32 x NB*4 floats
+  const long long red = (static_cast<long long>(geo.S / geo.kpw) + p.plan.csplit) * G * 32 * NB * 4 * 4;
   while (geo.stages * geo.stage < red) ++geo.stages;
   *smem_bytes = geo.stages * geo.stage + 2 * geo.stages * 8 + 16;
   return geo;

@@ -123,16 +123,31 @@ struct TcGeom {
   int tmem_cols;
 };
 
-template <int SCHEME>
+__device__ __forceinline__ uint32_t tc_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void tc_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// CS CTAs of a cluster split K for one 128-row block; their TMEM partials are summed through
+// distributed shared memory (each 16-column chunk has an owner rank, round robin).
+template <int SCHEME, int CS>
 __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams p, TcGeom geo) {
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, TK = T::kTK, J = T::kJ;
   constexpr int RUN = SCHEME == 7 ? 12 : 16;  // columns a lane emits per row and tile
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int blk = blockIdx.x;
+  const int blk = blockIdx.x / CS;
+  const uint32_t crank = CS > 1 ? tc_cluster_rank() : 0u;
   const int KT = p.k_tiles;
-  const int nst = (KT + geo.kchunk - 1) / geo.kchunk;
+  const int kper = (KT + CS - 1) / CS;
+  const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
+  const int nst = ke > kb ? (ke - kb + geo.kchunk - 1) / geo.kchunk : 0;
   uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
   uint64_t* fullB = fullA + geo.stages;
   uint64_t* empty = fullB + geo.stages;
@@ -185,8 +200,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     auto load_stage = [&](int st, uint4 (&v)[kMaxChunk], uint32_t (&sh)[kMaxChunk]) {
 #pragma unroll
       for (int kk = 0; kk < kMaxChunk; ++kk) {
-        const int kt = st * geo.kchunk + kk;
-        if (live && kk < geo.kchunk && kt < KT) {
+        const int kt = kb + st * geo.kchunk + kk;
+        if (live && kk < geo.kchunk && kt < ke) {
           const uint8_t* tp = wbase + kt * kstride;
           v[kk] = __ldcs(reinterpret_cast<const uint4*>(tp));
           sh[kk] = SCHEME == 4 ? __ldcs(tp + 512 - lane * 16 + lane) : 0u;
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       uint8_t* A = smem + sidx * geo.stage;
 #pragma unroll
       for (int kk = 0; kk < kMaxChunk; ++kk) {
-        if (kk < geo.kchunk && st * geo.kchunk + kk < KT) {
+        if (kk < geo.kchunk && kb + st * geo.kchunk + kk < ke) {
           uint32_t Af[J][4];
           const uint32_t R[4] = {cur[kk].x, cur[kk].y, cur[kk].z, cur[kk].w};
           uint32_t rowg[2 * J], rowg8[2 * J];  // a lane's RUN columns of rows g and g + 8
@@ -256,7 +271,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       uint32_t ph = 0;
       for (int st = 0; st < nst; ++st) {
         if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
-        const int kt0 = st * geo.kchunk, nk = min(geo.kchunk, KT - kt0);
+        const int kt0 = kb + st * geo.kchunk, nk = min(geo.kchunk, ke - kt0);
         const uint32_t bytes = static_cast<uint32_t>(nk * TK / 8) * lboB;
         mbar_arrive_expect_tx(&fullB[sidx], bytes);
         bulk_g2s(smem + sidx * geo.stage + geo.a_bytes,
@@ -277,7 +292,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
         mbar_wait(&fullA[sidx], ph);
         mbar_wait(&fullB[sidx], ph);
         tc_fence_after();
-        const int nk = min(geo.kchunk, KT - st * geo.kchunk);
+        const int nk = min(geo.kchunk, ke - (kb + st * geo.kchunk));
         const uint32_t a0 = smem_u32(smem + sidx * geo.stage);
         const uint32_t b0 = a0 + geo.a_bytes;
         for (int k16 = 0; k16 < nk * TK / 16; ++k16) {
@@ -293,23 +308,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   }
 
   // ------------------------------------------------------------------ epilogue
-  if (warp < kTcDecodeWarps) {
+  // warp w reads TMEM lanes 32*(w%4).. (its rows) for columns of half w/4, 16 at a time
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  const long long n = static_cast<long long>(blk) * 128 + row;
+  const int nchunks = p.Np / 16, ncap = (nchunks + CS - 1) / CS * 16;  // owned columns / rank
+  float* recv = reinterpret_cast<float*>(smem);  // [CS][128][ncap] (the idle stage ring)
+  auto store_y = [&](int m, float v) {
+    if (m < p.M && n < p.rows) {
+      const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+      p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
+    }
+  };
+  if (warp < kTcDecodeWarps && nst > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
+  }
+  if constexpr (CS > 1) {
+    // every rank's MMAs have finished reading its stage ring before any rank writes partials
+    // into a peer's (reused) ring
+    tc_fence_before();
+    tc_cluster_sync();
+    tc_fence_after();
+  } else {
     pdl_wait();  // y may still be read by the previous kernel
-    const int quarter = warp & 3, half = warp >> 2;
-    const long long n = static_cast<long long>(blk) * 128 + quarter * 32 + lane;
-    const float sc = n < p.rows ? __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale : 0.f;
-    const int cols_half = p.Np / 2;
-    for (int c0 = half * cols_half; c0 < (half + 1) * cols_half; c0 += 16) {
+  }
+  if (warp < kTcDecodeWarps) {
+    for (int c0 = half * (p.Np / 2); c0 < (half + 1) * (p.Np / 2); c0 += 16) {
       uint32_t v[16];
-      tc_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0), v);
+      if (nst > 0) {
+        tc_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0), v);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = c0 + j;
-        if (m < p.M && n < p.rows) {
-          p.y[static_cast<long long>(m) * p.ldy + n] =
-              __half_as_ushort(__float2half_rn(__uint_as_float(v[j]) * sc));
+        for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K range: a zero partial
+      }
+      if constexpr (CS == 1) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) store_y(c0 + j, __uint_as_float(v[j]));
+      } else {
+        const int ci = c0 / 16, owner = ci % CS, slot = (ci / CS) * 16;
+        float* dst = recv + (static_cast<long long>(crank) * 128 + row) * ncap + slot;
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(dst)), "r"(owner));
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(remote + j * 4),
+                       "r"(v[j]), "r"(v[j + 1]), "r"(v[j + 2]), "r"(v[j + 3])
+                       : "memory");
+        }
+      }
+    }
+  }
+  if constexpr (CS > 1) {
+    tc_fence_before();
+    tc_cluster_sync();  // all remote partials have landed
+    if (warp < kTcDecodeWarps) {
+      pdl_wait();
+      for (int c0 = half * (p.Np / 2); c0 < (half + 1) * (p.Np / 2); c0 += 16) {
+        const int ci = c0 / 16;
+        if (ci % CS != static_cast<int>(crank)) continue;
+        const int slot = (ci / CS) * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float v = 0.0f;
+#pragma unroll
+          for (int r = 0; r < CS; ++r) v += recv[(static_cast<long long>(r) * 128 + row) * ncap + slot + j];
+          store_y(c0 + j, v);  // rank order: deterministic
         }
       }
     }
@@ -325,6 +389,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 }  // namespace dev
 
 // ---------------------------------------------------------------- launchers
+template <int SCHEME, int CS>
+static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int smem, int rb,
+                               cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(rb * CS));
+  cfg.blockDim = dim3(dev::kTcThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int na = 1;
+  if constexpr (CS > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CS;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    na = 2;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME, CS>, p, geo);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <int SCHEME>
 static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long long ldx,
                                long long cols, cudaStream_t s) {
@@ -361,26 +458,21 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   geo.tmem_cols = 32;
   while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
   const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  // split K over a cluster when the 128-row blocks alone leave SMs idle
+  const int rb = (p.row_tiles + 7) / 8;
+  int cs = 1;
+  while (cs < 4 && rb * cs * 2 <= 148 && p.k_tiles >= 8 * cs * 2 &&
+         (cs * 2 != 4 || rb <= 32)) {
+    cs *= 2;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>((p.row_tiles + 7) / 8));
-  cfg.blockDim = dim3(dev::kTcThreads);
-  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME>, p, geo);
-  count_launch();
-  return e != cudaSuccess ? e : cudaGetLastError();
+  const int nchunks = p.Np / 16;
+  const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
+  if (cs > 1 && geo.stages * geo.stage < recv) cs = 1;
+  switch (cs) {
+    case 2: return launch_tc_m<SCHEME, 2>(p, geo, smem, rb, s);
+    case 4: return launch_tc_m<SCHEME, 4>(p, geo, smem, rb, s);
+    default: return launch_tc_m<SCHEME, 1>(p, geo, smem, rb, s);
+  }
 }
 
 cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
