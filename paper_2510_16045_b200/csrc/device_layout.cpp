@@ -7,6 +7,13 @@
 
 #include "host_core.hpp"
 
+#ifndef AMSQ_CLUSTER_COST_G  // plan cost of a cluster K split, in k-tiles (per row tile, fixed)
+#define AMSQ_CLUSTER_COST_G 1.0
+#endif
+#ifndef AMSQ_CLUSTER_COST_0
+#define AMSQ_CLUSTER_COST_0 3.0
+#endif
+
 namespace amsqb {
 
 bool device_scheme_supported(int id) { return id == 4 || id == 7; }
@@ -49,7 +56,7 @@ void choose_plan(size_t RT, size_t KT, DeviceLayout* L) {
       // a cluster's DSMEM reduction (remote stores of G row tiles' partials + one cluster
       // barrier) costs about one k-tile per row tile plus ~3 k-tiles of barrier latency
       const double work = static_cast<double>(G) * static_cast<double>((KT + C - 1) / C) +
-                          (C > 1 ? static_cast<double>(G) + 3.0 : 0.0);
+                          (C > 1 ? AMSQ_CLUSTER_COST_G * G + AMSQ_CLUSTER_COST_0 : 0.0);
       cands.push_back({work, static_cast<int>(ng) * C, C, static_cast<int>(ng),
                        static_cast<int>(G)});
     }

@@ -43,11 +43,15 @@
 
 namespace amsqb {
 
-constexpr int kPlanSMs = 148;   // B200 SM count the plan is built for
+#ifndef AMSQ_CTAS_PER_SM  // K2 CTAs resident per SM the plan is built for (1 in the product)
+#define AMSQ_CTAS_PER_SM 1
+#endif
+constexpr int kPlanSMs = 148 * AMSQ_CTAS_PER_SM;  // B200: 148 SMs
 // Clusters of C CTAs that can be co-resident (C = 1, 2, 4, 8; index by C). Larger clusters
 // must fit inside one GPC, which strands SMs: 4 -> 32 clusters, 8 -> 16 clusters assumed
 // (conservative; tools/cluster_probe reports the device's own figure).
-constexpr int kMaxClusters[9] = {0, 148, 74, 0, 32, 0, 0, 0, 16};
+constexpr int kMaxClusters[9] = {0, 148 * AMSQ_CTAS_PER_SM, 74 * AMSQ_CTAS_PER_SM, 0,
+                                 32 * AMSQ_CTAS_PER_SM, 0, 0, 0, 16 * AMSQ_CTAS_PER_SM};
 constexpr int kMaxGroupTiles = 64;  // 16 consumer warps x 4 row tiles each
 
 struct DeviceLayout {

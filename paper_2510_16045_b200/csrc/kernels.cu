@@ -170,6 +170,15 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_K2_WARPS
 #define AMSQ_K2_WARPS 16
 #endif
+#ifndef AMSQ_CTAS_PER_SM  // K2 CTAs per SM the plan assumes (device_layout.hpp); 1 in the product
+#define AMSQ_CTAS_PER_SM 1
+#endif
+#ifndef AMSQ_L2_PREFETCH  // pull the next ring's worth of weights into L2 ahead of the copies
+#define AMSQ_L2_PREFETCH 1
+#endif
+#ifndef AMSQ_TRACE_STAGES
+#define AMSQ_TRACE_STAGES 0
+#endif
 #ifndef AMSQ_K2_MODE  // profiling variants only (tools/build_variants.sh): 1 = stream only,
 #define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode
 #endif
@@ -232,7 +241,7 @@ __device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo,
 }
 
 template <int SCHEME, int NB, int CS>
-__global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams p, K2Geom geo) {
+__global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kernel(LinearParams p, K2Geom geo) {
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, J = T::kJ, TK = T::kTK, MS = 8 * NB, NB4 = NB * 4;
   constexpr bool kXPrep = NB == 2;
@@ -328,6 +337,20 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
                  static_cast<uint32_t>(n1 * G * TILE), &full[sidx], pol);
       }
     };
+    // DRAM latency under full load (~3 us) is longer than a ~200 KB ring can cover at the
+    // consumers' pace, so stage st + stages is pulled into L2 when stage st is issued: the
+    // ring's own copies then hit L2.
+    auto prefetch_w = [&](int st) {  // lane 0
+#if AMSQ_L2_PREFETCH
+      if (st >= nst) return;
+      int k0, n0, k1, n1;
+      runs(st, k0, n0, k1, n1);
+      bulk_prefetch_l2(wgrp + static_cast<long long>(k0) * G * TILE, static_cast<uint32_t>(n0 * G * TILE));
+      if (n1) bulk_prefetch_l2(wgrp + static_cast<long long>(k1) * G * TILE, static_cast<uint32_t>(n1 * G * TILE));
+#else
+      (void)st;
+#endif
+    };
     auto issue_x = [&](int st, int sidx) {  // whole warp; ends with arrival 2 of 2
       int k0, n0, k1, n1;
       runs(st, k0, n0, k1, n1);
@@ -379,7 +402,10 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
     // stage 0's weights do not depend on the previous kernel: request them before
     // griddepcontrol.wait. Later stages go weights-then-activations, so the TMA queue never
     // holds a ring's worth of weights in front of the activations the first stage needs.
-    if (lane == 0 && nst > 0) issue_w(0, 0);
+    if (lane == 0 && nst > 0) {
+      issue_w(0, 0);
+      for (int st = 1; st < 2 * geo.stages; ++st) prefetch_w(st);  // stages 1 .. 2*ring - 1
+    }
     pdl_wait();  // activations may be produced by the previous kernel
     if (trace && lane == 0) trace[4] = clock64();
     int sidx = 0;
@@ -387,9 +413,15 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
     for (int st = 0; st < nst; ++st) {
       if (st > 0) {
         if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
-        if (lane == 0) issue_w(st, sidx);
+        if (lane == 0) {
+          issue_w(st, sidx);
+          if (st >= geo.stages) prefetch_w(st + geo.stages);
+        }
       }
       issue_x(st, sidx);
+#if AMSQ_TRACE_STAGES
+      if (trace && lane == 0 && st < 24) trace[32 + st] = clock64();
+#endif
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
   } else {
@@ -447,6 +479,9 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
     for (int st = 0; st < nst; ++st) {
       mbar_wait(&full[sidx], ph);
       if (trace && st == 0 && threadIdx.x == 0) trace[1] = globaltimer();
+#if AMSQ_TRACE_STAGES  // profiling variant: stage landed (warp 0) / stage issued (producer)
+      if (trace && threadIdx.x == 0 && st < 24) trace[8 + st] = clock64();
+#endif
       const int nk = min(S, L - st * S);
       const uint8_t* sp = smem + sidx * geo.stage;
 #if AMSQ_K2_MODE == 1
@@ -461,6 +496,9 @@ __global__ void __launch_bounds__(kK2Threads, 1) amsq_linear_kernel(LinearParams
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sidx]);
+#if AMSQ_TRACE_STAGES
+      if (trace && warp == kConsumerWarps - 1 && lane == 0 && st < 7) trace[56 + st] = clock64();
+#endif
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
     if (trace && threadIdx.x == 0) trace[2] = globaltimer();
@@ -584,7 +622,7 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   geo.xrows = NB == 2 ? 16 : p.M;
   const int x_stage = NB == 2 ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
   geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
-  const int budget = 227 * 1024 - 1024;
+  const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024;
   geo.stages = budget / geo.stage;
   if (geo.stages > 6) geo.stages = 6;
   // the epilogue reuses the ring: (S/kpw + csplit) x G x 32 x NB*4 floats

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const int row = quarter * 32 + lane;
   const long long n = static_cast<long long>(blk) * 128 + row;
   const int nchunks = p.Np / 16, ncap = (nchunks + CS - 1) / CS * 16;  // owned columns / rank
+  const int nch_half = (nchunks + 1) / 2;  // 16-column chunks per epilogue warp half
   float* recv = reinterpret_cast<float*>(smem);  // [CS][128][ncap] (the idle stage ring)
   auto store_y = [&](int m, float v) {
     if (m < p.M && n < p.rows) {
@@ -334,7 +335,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     pdl_wait();  // y may still be read by the previous kernel
   }
   if (warp < kTcDecodeWarps) {
-    for (int c0 = half * (p.Np / 2); c0 < (half + 1) * (p.Np / 2); c0 += 16) {
+    for (int ci = half * nch_half; ci < min(nchunks, (half + 1) * nch_half); ++ci) {
+      const int c0 = ci * 16;
       uint32_t v[16];
       if (nst > 0) {
         tc_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0), v);
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 #pragma unroll
         for (int j = 0; j < 16; ++j) store_y(c0 + j, __uint_as_float(v[j]));
       } else {
-        const int ci = c0 / 16, owner = ci % CS, slot = (ci / CS) * 16;
+        const int owner = ci % CS, slot = (ci / CS) * 16;
         float* dst = recv + (static_cast<long long>(crank) * 128 + row) * ncap + slot;
         uint32_t remote;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(dst)), "r"(owner));
@@ -364,8 +366,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     tc_cluster_sync();  // all remote partials have landed
     if (warp < kTcDecodeWarps) {
       pdl_wait();
-      for (int c0 = half * (p.Np / 2); c0 < (half + 1) * (p.Np / 2); c0 += 16) {
-        const int ci = c0 / 16;
+      for (int ci = half * nch_half; ci < min(nchunks, (half + 1) * nch_half); ++ci) {
+        const int c0 = ci * 16;
         if (ci % CS != static_cast<int>(crank)) continue;
         const int slot = (ci / CS) * 16;
 #pragma unroll

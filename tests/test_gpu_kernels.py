@@ -200,3 +200,17 @@ def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch):
     yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
     _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
     check_linear(y, yref, yabs)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("batch", [17, 48, 112, 144, 200])
+def test_linear_tcgen05_cluster_split_odd_chunks(cuda, orc, sid, batch):
+    """K3 with a 2/4-CTA K split and a batch whose 16-column chunk count is odd."""
+    rows, cols = 512, 2048 if sid == 4 else 2049
+    qt = quantized_gaussian(sid, rows, cols, seed=batch)
+    x = gaussian_x(batch, cols, seed=batch + 1)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)

@@ -34,10 +34,12 @@ print("  start      ", q(st)); print("  first stage", q(first)); print("  stream
 print("  first-stage latency per CTA", q(first - st), " epilogue per CTA", q(end - loop))
 GHZ = 1.9  # SM clock under this load (clocks.sm ~1965 MHz); stamps 4.. are clock64
 clk = lambda c, v: st[c] + (v - t[c, 63]) / GHZ / 1e3
-print("  producer stamps (CTA 0): after pdl_wait + x issues:",
-      " ".join(f"{clk(0, t[0, 4 + i]):.2f}" for i in range(4) if t[0, 4 + i] > 0))
+print("  producer: after pdl_wait (CTA 0):", f"{clk(0, t[0, 4]):.2f}")
 for c in (0, len(t) // 2):
-    land = [clk(c, t[c, 8 + 2 * s]) for s in range(28) if t[c, 8 + 2 * s] > 0]
-    done = [clk(c, t[c, 9 + 2 * s]) for s in range(28) if t[c, 9 + 2 * s] > 0]
-    print(f"  CTA {c}: start {st[c]:.2f}; stage landed/consumed:",
-          " ".join(f"{l:.2f}/{d:.2f}" for l, d in zip(land, done)))
+    land = [clk(c, t[c, 8 + s]) for s in range(24) if t[c, 8 + s] > 0]
+    iss = [clk(c, t[c, 32 + s]) for s in range(24) if t[c, 32 + s] > 0]
+    last = [clk(c, t[c, 56 + s]) for s in range(7) if t[c, 56 + s] > 0]
+    print(f"  CTA {c}: start {st[c]:.2f}")
+    print("    x issued :", " ".join(f"{v:.2f}" for v in iss))
+    print("    landed   :", " ".join(f"{v:.2f}" for v in land))
+    print("    last warp done:", " ".join(f"{v:.2f}" for v in last))
