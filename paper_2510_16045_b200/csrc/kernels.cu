@@ -173,8 +173,11 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_CTAS_PER_SM  // K2 CTAs per SM the plan assumes (device_layout.hpp); 1 in the product
 #define AMSQ_CTAS_PER_SM 1
 #endif
+#ifndef AMSQ_OWN_TARGET  // row tiles per consumer warp the stage geometry aims for (<= 4)
+#define AMSQ_OWN_TARGET 4
+#endif
 #ifndef AMSQ_L2_PREFETCH  // pull the next ring's worth of weights into L2 ahead of the copies
-#define AMSQ_L2_PREFETCH 1
+#define AMSQ_L2_PREFETCH 0
 #endif
 #ifndef AMSQ_TRACE_STAGES
 #define AMSQ_TRACE_STAGES 0
@@ -607,7 +610,7 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   // (<= 4 when even all warps on one k-slot cannot)
   int wr = dev::kConsumerWarps;
   for (int d = 1; d <= dev::kConsumerWarps; ++d) {
-    if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= 2) {
+    if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= AMSQ_OWN_TARGET) {
       wr = d;
       break;
     }

@@ -111,8 +111,10 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-constexpr int kTcDecodeWarps = 8;
+constexpr int kTcDecodeWarps = 16;  // two per row tile (even / odd k-tiles of each stage)
+constexpr int kTcEpiWarps = 8;      // the epilogue's TMEM readers (4 lane quarters x 2 halves)
 constexpr int kTcThreads = (kTcDecodeWarps + 2) * 32;  // + B producer + MMA issuer
+constexpr int kTcRing = 4;          // per-warp cp.async weight ring depth (stages)
 
 struct TcGeom {
   int kchunk;   // k-tiles per stage
@@ -121,6 +123,7 @@ struct TcGeom {
   int b_bytes;  // B buffer per stage: Np rows x kchunk*TK fp16
   int stage;    // a_bytes + b_bytes (128-aligned)
   int tmem_cols;
+  int ring;     // per decode warp: kTcRing stages x kchunk/2 tiles (bytes, 128-aligned)
 };
 
 __device__ __forceinline__ uint32_t tc_cluster_rank() {
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const int kper = (KT + CS - 1) / CS;
   const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
   const int nst = ke > kb ? (ke - kb + geo.kchunk - 1) / geo.kchunk : 0;
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
+  uint8_t* rings = smem + geo.stages * geo.stage;  // [kTcDecodeWarps][ring]
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(rings + kTcDecodeWarps * geo.ring);
   uint64_t* fullB = fullA + geo.stages;
   uint64_t* empty = fullB + geo.stages;
   uint64_t* done = empty + geo.stages;
@@ -178,80 +182,93 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 
   if (warp < kTcDecodeWarps) {
     // ------------------------------------------------------------------ decode warps
-    const int rt = blk * 8 + warp;
+    // warp w: row tile 8*blk + (w & 7), the k-tiles of parity w >> 3 of every stage. Its
+    // tiles stream through a private kTcRing-deep cp.async ring (one commit group per stage)
+    // so ~kTcRing stages of weights are in flight per warp without holding registers.
+    const int rt = blk * 8 + (warp & 7), par = warp >> 3;
     const bool live = rt < p.row_tiles;
     const int g = lane >> 2, t = lane & 3;
-    long long toff[2] = {0, 0};  // not used: tile offsets computed per k-tile
-    (void)toff;
     const GroupPlan& P = p.plan;
-    int grp = 0, G = 1, r0 = 0;
+    int G = 1, r0 = 0;
     if (live) {
       const int big_rows = P.n_big * P.g_big;
-      grp = rt < big_rows ? rt / P.g_big : P.n_big + (rt - big_rows) / (P.g_big - 1);
+      const int grp = rt < big_rows ? rt / P.g_big : P.n_big + (rt - big_rows) / (P.g_big - 1);
       G = P.size(grp);
       r0 = P.row0(grp);
     }
     // tile (rt, kt) lives at ((r0 * KT) + kt * G + (rt - r0)) * TILE (device_layout.hpp)
-    const uint8_t* wbase = p.w + (static_cast<long long>(r0) * KT + (rt - r0)) * TILE + lane * 16;
+    const uint8_t* tbase = p.w + (static_cast<long long>(r0) * KT + (rt - r0)) * TILE;
     const long long kstride = static_cast<long long>(G) * TILE;
-    constexpr int kMaxChunk = 4;
-    uint4 cur[kMaxChunk], nxt[kMaxChunk];
-    uint32_t shc[kMaxChunk], shn[kMaxChunk];
-    auto load_stage = [&](int st, uint4 (&v)[kMaxChunk], uint32_t (&sh)[kMaxChunk]) {
-#pragma unroll
-      for (int kk = 0; kk < kMaxChunk; ++kk) {
-        const int kt = kb + st * geo.kchunk + kk;
-        if (live && kk < geo.kchunk && kt < ke) {
-          const uint8_t* tp = wbase + kt * kstride;
-          v[kk] = __ldcs(reinterpret_cast<const uint4*>(tp));
-          sh[kk] = SCHEME == 4 ? __ldcs(tp + 512 - lane * 16 + lane) : 0u;
-        } else {
-          v[kk] = make_uint4(0, 0, 0, 0);
-          sh[kk] = 0;
+    const int half_chunk = geo.kchunk / 2;
+    uint8_t* ring = rings + warp * geo.ring;
+    auto issue = [&](int st) {
+      if (st < nst) {
+        uint8_t* slot = ring + (st % kTcRing) * half_chunk * TILE;
+        for (int j = 0; j < half_chunk; ++j) {
+          const int kt = kb + st * geo.kchunk + 2 * j + par;
+          if (live && kt < ke) {
+            const uint8_t* src = tbase + kt * kstride;
+            cp_async_16(slot + j * TILE + lane * 16, src + lane * 16, 16);
+            if (SCHEME == 4 && lane < 2) cp_async_16(slot + j * TILE + 512 + lane * 16, src + 512 + lane * 16, 16);
+          }
         }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (nst > 0) load_stage(0, cur, shc);
+    for (int st = 0; st < kTcRing - 1; ++st) issue(st);
     int sidx = 0;
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
-      if (st + 1 < nst) load_stage(st + 1, nxt, shn);  // prefetch the next stage
+      issue(st + kTcRing - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kTcRing - 1) : "memory");
+      __syncwarp();
       if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
       uint8_t* A = smem + sidx * geo.stage;
-#pragma unroll
-      for (int kk = 0; kk < kMaxChunk; ++kk) {
-        if (kk < geo.kchunk && kb + st * geo.kchunk + kk < ke) {
+      const uint8_t* slot = ring + (st % kTcRing) * half_chunk * TILE;
+      for (int j = 0; j < half_chunk; ++j) {
+        const int kk = 2 * j + par;
+        if (kb + st * geo.kchunk + kk < ke) {
+          uint4 wv = make_uint4(0, 0, 0, 0);
+          uint32_t sh = 0;
+          if (live) {
+            wv = *reinterpret_cast<const uint4*>(slot + j * TILE + lane * 16);
+            if (SCHEME == 4) sh = slot[j * TILE + 512 + lane];
+          }
           uint32_t Af[J][4];
-          const uint32_t R[4] = {cur[kk].x, cur[kk].y, cur[kk].z, cur[kk].w};
+          const uint32_t R[4] = {wv.x, wv.y, wv.z, wv.w};
           uint32_t rowg[2 * J], rowg8[2 * J];  // a lane's RUN columns of rows g and g + 8
           if constexpr (SCHEME == 4) {
-            decode_s4(R, shc[kk], Af);
+            decode_s4(R, sh, Af);
             // A[j] = {g:(16t+j,16t+4+j), g+8, g:(16t+8+j,16t+12+j), g+8}: emit q-major
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              rowg[j] = Af[j][0], rowg[4 + j] = Af[j][2];
-              rowg8[j] = Af[j][1], rowg8[4 + j] = Af[j][3];
+            for (int jj = 0; jj < 4; ++jj) {
+              rowg[jj] = Af[jj][0], rowg[4 + jj] = Af[jj][2];
+              rowg8[jj] = Af[jj][1], rowg8[4 + jj] = Af[jj][3];
             }
           } else {
             decode_s7(R, Af);
             // A[j] = {g: pair 2j, g+8: pair 2j, g: pair 2j+1, g+8: pair 2j+1}
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              rowg[2 * j] = Af[j][0], rowg[2 * j + 1] = Af[j][2];
-              rowg8[2 * j] = Af[j][1], rowg8[2 * j + 1] = Af[j][3];
+            for (int jj = 0; jj < 3; ++jj) {
+              rowg[2 * jj] = Af[jj][0], rowg[2 * jj + 1] = Af[jj][2];
+              rowg8[2 * jj] = Af[jj][1], rowg8[2 * jj + 1] = Af[jj][3];
             }
           }
           // [k/8][128][8] image: column c of row r at (c / 8) * lboA + r * 16 + (c % 8) * 2
           const int c0 = kk * TK + RUN * t;  // first (permuted) column of the run
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int r = warp * 16 + g + 8 * h;
+            const int r = (warp & 7) * 16 + g + 8 * h;
             const uint32_t* v = h ? rowg8 : rowg;
-#pragma unroll
-            for (int q = 0; q < RUN / 4; ++q) {  // 8-byte pieces (4 columns)
-              const int c = c0 + 4 * q;
-              *reinterpret_cast<uint2*>(A + (c >> 3) * lboA + r * 16 + (c & 7) * 2) =
-                  make_uint2(v[2 * q], v[2 * q + 1]);
+            if constexpr (RUN == 16) {  // two whole 8-column core rows
+              *reinterpret_cast<uint4*>(A + (c0 >> 3) * lboA + r * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+              *reinterpret_cast<uint4*>(A + ((c0 >> 3) + 1) * lboA + r * 16) = make_uint4(v[4], v[5], v[6], v[7]);
+            } else if ((t & 1) == 0) {  // 12 columns from a core-row boundary: 8 + 4
+              *reinterpret_cast<uint4*>(A + (c0 >> 3) * lboA + r * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+              *reinterpret_cast<uint2*>(A + ((c0 >> 3) + 1) * lboA + r * 16) = make_uint2(v[4], v[5]);
+            } else {  // 4 + 8
+              *reinterpret_cast<uint2*>(A + (c0 >> 3) * lboA + r * 16 + 8) = make_uint2(v[0], v[1]);
+              *reinterpret_cast<uint4*>(A + ((c0 >> 3) + 1) * lboA + r * 16) = make_uint4(v[2], v[3], v[4], v[5]);
             }
           }
         }
@@ -259,10 +276,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sidx]);
-#pragma unroll
-      for (int kk = 0; kk < kMaxChunk; ++kk) cur[kk] = nxt[kk], shc[kk] = shn[kk];
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kTcDecodeWarps) {
     // ------------------------------------------------------------------ B producer
     if (lane == 0) {
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
     }
   };
-  if (warp < kTcDecodeWarps && nst > 0) {
+  if (warp < kTcEpiWarps && nst > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
   }
@@ -334,7 +350,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   } else {
     pdl_wait();  // y may still be read by the previous kernel
   }
-  if (warp < kTcDecodeWarps) {
+  if (warp < kTcEpiWarps) {
     for (int ci = half * nch_half; ci < min(nchunks, (half + 1) * nch_half); ++ci) {
       const int c0 = ci * 16;
       uint32_t v[16];
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   if constexpr (CS > 1) {
     tc_fence_before();
     tc_cluster_sync();  // all remote partials have landed
-    if (warp < kTcDecodeWarps) {
+    if (warp < kTcEpiWarps) {
       pdl_wait();
       for (int ci = half * nch_half; ci < min(nchunks, (half + 1) * nch_half); ++ci) {
         const int c0 = ci * 16;
@@ -446,20 +462,21 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
     if (e != cudaSuccess) return e;
   }
   dev::TcGeom geo{};
-  const int budget = 220 * 1024;
-  for (int kc : {4, 2, 1}) {
+  const int budget = 227 * 1024 - 512;
+  for (int kc : {4, 2}) {
     geo.kchunk = kc;
     geo.a_bytes = 128 * kc * T::kTK * 2;
     geo.b_bytes = p.Np * kc * T::kTK * 2;
     geo.stage = (geo.a_bytes + geo.b_bytes + 1023) / 1024 * 1024;
-    geo.stages = budget / geo.stage;
+    geo.ring = (dev::kTcRing * (kc / 2) * T::kTileBytes + 127) / 128 * 128;
+    geo.stages = (budget - dev::kTcDecodeWarps * geo.ring) / geo.stage;
     if (geo.stages >= 3) break;
   }
   if (geo.stages > 6) geo.stages = 6;
   if (geo.stages < 2) return cudaErrorInvalidConfiguration;
   geo.tmem_cols = 32;
   while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
-  const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16;
+  const int smem = geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring + (3 * geo.stages + 1) * 8 + 16;
   // split K over a cluster when the 128-row blocks alone leave SMs idle
   const int rb = (p.row_tiles + 7) / 8;
   int cs = 1;
@@ -469,7 +486,7 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   }
   const int nchunks = p.Np / 16;
   const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
-  if (cs > 1 && geo.stages * geo.stage < recv) cs = 1;
+  if (cs > 1 && geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring < recv) cs = 1;
   switch (cs) {
     case 2: return launch_tc_m<SCHEME, 2>(p, geo, smem, rb, s);
     case 4: return launch_tc_m<SCHEME, 4>(p, geo, smem, rb, s);
