@@ -298,11 +298,18 @@ def run_ours(args, world, rank, local):
                 extra[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
         extra["extra_seconds"] = round(time.time() - t, 1)
 
-    traffic = None
+    # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of the
+    # dominant launch (profiles/ncu_traffic.json), per launch, beside its algorithmic bytes
+    traffic, traffic_note = None, None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.scheme)
+            rec = json.load(open(tfile)).get(args.scheme)
+            if rec:
+                traffic = rec["traffic_bytes_per_launch"]
+                traffic_note = (f"{rec['launch']}: dram {rec['traffic_bytes_per_launch']} B vs "
+                                f"algorithmic {rec['algorithmic_bytes_per_launch']} B "
+                                f"(ratio {rec['ratio']})")
         except Exception:
             traffic = None
 
@@ -323,6 +330,7 @@ def run_ours(args, world, rank, local):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_note": traffic_note,
                      "kernel": "amsq_linear_kernel", "peak_kind": peak_kind,
                      "bytes": "algorithmic = packed_payload_bytes + 2N + 2MK + 2MN per call"},
         "gpu_launches": int(launches),

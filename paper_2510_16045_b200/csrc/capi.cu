@@ -198,6 +198,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     q.row_tiles = p.row_tiles;
     q.k_tiles = p.k_tiles;
     q.plan = p.plan;
+    q.trace = g_trace;
     for (size_t b0 = 0; b0 < batch; b0 += amsqb::kTcMaxBatch) {
       const size_t mb = batch - b0 < static_cast<size_t>(amsqb::kTcMaxBatch) ? batch - b0 : amsqb::kTcMaxBatch;
       q.M = static_cast<int>(mb);

@@ -11,7 +11,7 @@
 #define AMSQ_CLUSTER_COST_G 1.0
 #endif
 #ifndef AMSQ_CLUSTER_COST_0
-#define AMSQ_CLUSTER_COST_0 3.0
+#define AMSQ_CLUSTER_COST_0 25.0  // cluster barrier + DSMEM epilogue ~0.6 us (o_proj: C=1 wins)
 #endif
 
 namespace amsqb {
@@ -56,8 +56,8 @@ void choose_plan(size_t RT, size_t KT, DeviceLayout* L) {
       // a cluster's DSMEM reduction (remote stores of G row tiles' partials + one cluster
       // barrier) costs about one k-tile per row tile plus ~3 k-tiles of barrier latency
       // a consumer warp reuses each k-tile's activation fragments over its <= 4 row tiles:
-      // with fewer than 4 row tiles per CTA the per-byte cost rises (measured: 2 tiles ~1.3x)
-      const double reuse = 1.0 + 0.6 * (4.0 - static_cast<double>(std::min<size_t>(G, 4))) / 4.0;
+      // with fewer than 4 row tiles per CTA the per-byte cost rises (measured: 2 tiles ~1.15x)
+      const double reuse = 1.0 + 0.3 * (4.0 - static_cast<double>(std::min<size_t>(G, 4))) / 4.0;
       const double work = static_cast<double>(G) * static_cast<double>((KT + C - 1) / C) * reuse +
                           (C > 1 ? AMSQ_CLUSTER_COST_G * G + AMSQ_CLUSTER_COST_0 : 0.0);
       cands.push_back({work, static_cast<int>(ng) * C, C, static_cast<int>(ng),

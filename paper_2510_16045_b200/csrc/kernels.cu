@@ -173,6 +173,9 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_CTAS_PER_SM  // K2 CTAs per SM the plan assumes (device_layout.hpp); 1 in the product
 #define AMSQ_CTAS_PER_SM 1
 #endif
+#ifndef AMSQ_K2_XPREP  // 1: M <= 16 reads activations pre-permuted by amsq_xprep_kernel (an extra
+#define AMSQ_K2_XPREP 1  // launch); 0: natural rows + PRMT like M <= 8 (measured slower)
+#endif
 #ifndef AMSQ_OWN_TARGET  // row tiles per consumer warp the stage geometry aims for (<= 4)
 #define AMSQ_OWN_TARGET 4
 #endif
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode
 #endif
 constexpr int kConsumerWarps = AMSQ_K2_WARPS;
+constexpr bool kK2XPrep = AMSQ_K2_XPREP != 0;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
 constexpr int kMaxOwn = 4;                              // row tiles per consumer warp
 
@@ -216,7 +220,7 @@ __device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo,
   constexpr int J = T::kJ, MS = 8 * NB;
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    if constexpr (NB == 2) {
+    if constexpr (kK2XPrep && NB == 2) {
       const uint2* xu = reinterpret_cast<const uint2*>(xs) + ((ks * J) * MS + nb * 8 + g) * 4 + t;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
@@ -226,7 +230,8 @@ __device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo,
       }
     } else {
       // batch rows >= M only feed accumulator columns that are never stored: read row M-1
-      const uint8_t* xp = xs + min(g, geo.xrows - 1) * geo.x_row + (ks * T::kTK + t * T::kLaneK) * 2;
+      const uint8_t* xp =
+          xs + min(nb * 8 + g, geo.xrows - 1) * geo.x_row + (ks * T::kTK + t * T::kLaneK) * 2;
       if constexpr (SCHEME == 4) {
         const uint4 a = *reinterpret_cast<const uint4*>(xp);
         const uint4 b = *reinterpret_cast<const uint4*>(xp + 16);
@@ -247,7 +252,7 @@ template <int SCHEME, int NB, int CS>
 __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kernel(LinearParams p, K2Geom geo) {
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, J = T::kJ, TK = T::kTK, MS = 8 * NB, NB4 = NB * 4;
-  constexpr bool kXPrep = NB == 2;
+  constexpr bool kXPrep = kK2XPrep && NB == 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -622,8 +627,8 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const int x_raw = geo.S * T::kTK * 2;
   const int target = SCHEME == 7 ? 96 : 16;  // lanes' LDS hit distinct banks
   geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
-  geo.xrows = NB == 2 ? 16 : p.M;
-  const int x_stage = NB == 2 ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
+  geo.xrows = (dev::kK2XPrep && NB == 2) ? 16 : p.M;
+  const int x_stage = (dev::kK2XPrep && NB == 2) ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
   geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
   const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024;
   geo.stages = budget / geo.stage;
@@ -672,7 +677,7 @@ static cudaError_t launch_linear_m(const LinearParams& p, cudaStream_t s) {
 
 template <int SCHEME, int NB>
 static cudaError_t launch_linear_t(const LinearParams& p, cudaStream_t s) {
-  if constexpr (NB == 2) {
+  if constexpr (NB == 2 && dev::kK2XPrep) {
     // activations first (PDL-chained: waits for whoever produced x, lets the linear start
     // streaming weights as soon as it is scheduled)
     const int MS = 8 * NB;

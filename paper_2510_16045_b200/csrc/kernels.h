@@ -55,6 +55,7 @@ struct TcParams {
   int M, Np;                 // batch rows; Np = round_up(M, 16) <= 256
   int row_tiles, k_tiles;
   GroupPlan plan;
+  unsigned long long* trace;  // profiling only: per-CTA globaltimer stamps (null = off)
 };
 
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);

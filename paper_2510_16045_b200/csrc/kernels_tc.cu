@@ -4,16 +4,17 @@
 //
 // Swap-AB: D[128 weight rows][Np batch] += W[128 x K] . X^T[K x Np], D in TMEM (128 lanes x
 // Np fp32 columns), one CTA per 128-row block (8 row tiles of the tile layout).
-//  * warps 0..7 ("decode"): warp w streams row tile 8*blk + w straight from HBM (one LDG.128
-//    per lane per tile, the next stage prefetched), decodes in registers (the same
-//    decode_s4 / decode_s7 as K2) and stores the placed fp16 pairs into the stage's A
-//    buffer in the UMMA canonical K-major no-swizzle layout [k/8][128 rows][8];
+//  * warps 0..15 ("decode"): two per row tile (even / odd k-tiles of each stage); each
+//    streams its tiles from HBM through a private 4-deep cp.async ring, decodes in registers
+//    (the same decode_s4 / decode_s7 as K2) and stores the placed fp16 pairs into the stage's
+//    A buffer in the UMMA canonical K-major no-swizzle layout [k/8][128 rows][8];
 //    fence.proxy.async + one mbarrier arrival per warp.
-//  * warp 8 ("B producer"): one cp.async.bulk per stage of the activations, prepped once per
+//  * warp 16 ("B producer"): one cp.async.bulk per stage of the activations, prepped once per
 //    call by amsq_xprep_tc_kernel into the same [k/8][Np][8] image; owns the TMEM allocation.
-//  * warp 9 ("MMA"): one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
+//  * warp 17 ("MMA"): one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
 //    N=Np, K=16) per 16 columns and tcgen05.commit's the stage back to the producers.
-//  * epilogue (warps 0..7): tcgen05.ld 32x32b -> fp32 * scale * 2^14 -> fp16 y.
+//  * epilogue (warps 0..7): tcgen05.ld 32x32b -> fp32 * scale * 2^14 -> fp16 y; a cluster of
+//    2/4 CTAs that split K sums its TMEM partials through DSMEM first.
 // The decode emits a lane's fp16 pairs in its own order, so the K axis is permuted inside
 // every tile column chunk (tc_kperm); the activation prep applies the same permutation, so
 // the contraction is unchanged. Accumulation order: k ascending per MMA -- deterministic.
@@ -21,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.h"
 #include "kernels_common.cuh"
@@ -114,7 +116,7 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 constexpr int kTcDecodeWarps = 16;  // two per row tile (even / odd k-tiles of each stage)
 constexpr int kTcEpiWarps = 8;      // the epilogue's TMEM readers (4 lane quarters x 2 halves)
 constexpr int kTcThreads = (kTcDecodeWarps + 2) * 32;  // + B producer + MMA issuer
-constexpr int kTcRing = 4;          // per-warp cp.async weight ring depth (stages)
+
 
 struct TcGeom {
   int kchunk;   // k-tiles per stage
@@ -123,7 +125,8 @@ struct TcGeom {
   int b_bytes;  // B buffer per stage: Np rows x kchunk*TK fp16
   int stage;    // a_bytes + b_bytes (128-aligned)
   int tmem_cols;
-  int ring;     // per decode warp: kTcRing stages x kchunk/2 tiles (bytes, 128-aligned)
+  int ring;     // per decode warp: RING stages x kchunk/2 tiles (bytes, 128-aligned)
+  int ring_deep;  // ring depth in stages (8, 4 or 2: the deepest that fits)
 };
 
 __device__ __forceinline__ uint32_t tc_cluster_rank() {
@@ -138,8 +141,9 @@ __device__ __forceinline__ void tc_cluster_sync() {
 
 // CS CTAs of a cluster split K for one 128-row block; their TMEM partials are summed through
 // distributed shared memory (each 16-column chunk has an owner rank, round robin).
-template <int SCHEME, int CS>
+template <int SCHEME, int CS, int RING>
 __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams p, TcGeom geo) {
+  constexpr int kTcRing = RING;  // per-warp cp.async weight ring depth (stages)
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, TK = T::kTK, J = T::kJ;
   constexpr int RUN = SCHEME == 7 ? 12 : 16;  // columns a lane emits per row and tile
@@ -156,9 +160,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   uint64_t* fullB = fullA + geo.stages;
   uint64_t* empty = fullB + geo.stages;
   uint64_t* done = empty + geo.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* rbar = done + 1;  // [kTcDecodeWarps][RING] weight-ring slot barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kTcDecodeWarps * RING);
   const uint32_t lboA = 128 * 16, lboB = static_cast<uint32_t>(p.Np) * 16;
 
+  unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < geo.stages; ++s) {
@@ -167,6 +174,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    for (int i = 0; i < kTcDecodeWarps * RING; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == kTcDecodeWarps) {  // TMEM: Np fp32 columns x 128 lanes
@@ -201,27 +209,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     const long long kstride = static_cast<long long>(G) * TILE;
     const int half_chunk = geo.kchunk / 2;
     uint8_t* ring = rings + warp * geo.ring;
-    auto issue = [&](int st) {
-      if (st < nst) {
-        uint8_t* slot = ring + (st % kTcRing) * half_chunk * TILE;
-        for (int j = 0; j < half_chunk; ++j) {
-          const int kt = kb + st * geo.kchunk + 2 * j + par;
-          if (live && kt < ke) {
-            const uint8_t* src = tbase + kt * kstride;
-            cp_async_16(slot + j * TILE + lane * 16, src + lane * 16, 16);
-            if (SCHEME == 4 && lane < 2) cp_async_16(slot + j * TILE + 512 + lane * 16, src + 512 + lane * 16, 16);
-          }
+    // slot refills go through the bulk engine (one copy per tile, completion on the slot's
+    // mbarrier): the per-stage fence.proxy.async below would otherwise wait for this
+    // thread's outstanding cp.async (LDGSTS) and serialise the ring
+    uint64_t* mybar = rbar + warp * kTcRing;
+    auto issue = [&](int st) {  // lane 0
+      if (st >= nst) return;
+      const int si = st % kTcRing;
+      uint8_t* slot = ring + si * half_chunk * TILE;
+      uint32_t bytes = 0;
+      for (int j = 0; j < half_chunk; ++j) {
+        const int kt = kb + st * geo.kchunk + 2 * j + par;
+        if (live && kt < ke) bytes += TILE;
+      }
+      mbar_arrive_expect_tx(&mybar[si], bytes);
+      for (int j = 0; j < half_chunk; ++j) {
+        const int kt = kb + st * geo.kchunk + 2 * j + par;
+        if (live && kt < ke) {
+          bulk_g2s(slot + j * TILE, tbase + kt * kstride, TILE, &mybar[si], policy_evict_first());
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int st = 0; st < kTcRing - 1; ++st) issue(st);
+    if (lane == 0) {
+      for (int st = 0; st < kTcRing - 1; ++st) issue(st);
+    }
     int sidx = 0;
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
-      issue(st + kTcRing - 1);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kTcRing - 1) : "memory");
-      __syncwarp();
+      if (lane == 0) issue(st + kTcRing - 1);
+      mbar_wait(&mybar[st % kTcRing], (st / kTcRing) & 1);
       if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
       uint8_t* A = smem + sidx * geo.stage;
       const uint8_t* slot = ring + (st % kTcRing) * half_chunk * TILE;
@@ -276,9 +292,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sidx]);
+      if (trace && warp == 0 && lane == 0 && st < 24) trace[8 + st] = globaltimer();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kTcDecodeWarps) {
     // ------------------------------------------------------------------ B producer
     if (lane == 0) {
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           tc_mma_f16(tmem, ad, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
         }
         tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
+        if (trace && st < 24) trace[32 + st] = globaltimer();
         if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
       }
       tc_commit(done);
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const long long n = static_cast<long long>(blk) * 128 + row;
   const int nchunks = p.Np / 16, ncap = (nchunks + CS - 1) / CS * 16;  // owned columns / rank
   const int nch_half = (nchunks + 1) / 2;  // 16-column chunks per epilogue warp half
-  float* recv = reinterpret_cast<float*>(smem);  // [CS][128][ncap] (the idle stage ring)
+  float* recv = reinterpret_cast<float*>(smem);  // [CS][ncap][128] (the idle stage ring)
   auto store_y = [&](int m, float v) {
     if (m < p.M && n < p.rows) {
       const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
@@ -341,6 +358,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     mbar_wait(done, 0);
     tc_fence_after();
   }
+  if (trace && threadIdx.x == 0) trace[2] = globaltimer();
   if constexpr (CS > 1) {
     // every rank's MMAs have finished reading its stage ring before any rank writes partials
     // into a peer's (reused) ring
@@ -365,13 +383,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
         for (int j = 0; j < 16; ++j) store_y(c0 + j, __uint_as_float(v[j]));
       } else {
         const int owner = ci % CS, slot = (ci / CS) * 16;
-        float* dst = recv + (static_cast<long long>(crank) * 128 + row) * ncap + slot;
+        // [rank][column][row]: consecutive lanes (rows) hit consecutive banks
+        float* dst = recv + (static_cast<long long>(crank) * ncap + slot) * 128 + row;
         uint32_t remote;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(dst)), "r"(owner));
 #pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(remote + j * 4),
-                       "r"(v[j]), "r"(v[j + 1]), "r"(v[j + 2]), "r"(v[j + 3])
+        for (int j = 0; j < 16; ++j) {
+          asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(remote + j * 128 * 4), "r"(v[j])
                        : "memory");
         }
       }
@@ -390,12 +408,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
         for (int j = 0; j < 16; ++j) {
           float v = 0.0f;
 #pragma unroll
-          for (int r = 0; r < CS; ++r) v += recv[(static_cast<long long>(r) * 128 + row) * ncap + slot + j];
+          for (int r = 0; r < CS; ++r) v += recv[(static_cast<long long>(r) * ncap + slot + j) * 128 + row];
           store_y(c0 + j, v);  // rank order: deterministic
         }
       }
     }
   }
+  if (trace && threadIdx.x == 0) trace[3] = globaltimer();
   tc_fence_before();
   __syncthreads();
   if (warp == kTcDecodeWarps) {
@@ -407,12 +426,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 }  // namespace dev
 
 // ---------------------------------------------------------------- launchers
-template <int SCHEME, int CS>
+template <int SCHEME, int CS, int RING>
 static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int smem, int rb,
                                cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS>,
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS, RING>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -435,7 +454,7 @@ static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int sm
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME, CS>, p, geo);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME, CS, RING>, p, geo);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -461,22 +480,31 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
     count_launch();
     if (e != cudaSuccess) return e;
   }
-  dev::TcGeom geo{};
-  const int budget = 227 * 1024 - 512;
-  for (int kc : {4, 2}) {
-    geo.kchunk = kc;
-    geo.a_bytes = 128 * kc * T::kTK * 2;
-    geo.b_bytes = p.Np * kc * T::kTK * 2;
-    geo.stage = (geo.a_bytes + geo.b_bytes + 1023) / 1024 * 1024;
-    geo.ring = (dev::kTcRing * (kc / 2) * T::kTileBytes + 127) / 128 * 128;
-    geo.stages = (budget - dev::kTcDecodeWarps * geo.ring) / geo.stage;
-    if (geo.stages >= 3) break;
+  dev::TcGeom geo{}, best{};
+  best.stages = 0;
+  const int budget = 227 * 1024 - 2048;
+  // prefer a deep (8-stage) per-warp weight ring (it sets the bytes in flight per SM) and
+  // >= 3 A/B stages; otherwise the configuration with the most A/B stages
+  for (int depth : {8, 4, 2}) {
+    for (int kc : {2, 4}) {
+      geo.kchunk = kc;
+      geo.a_bytes = 128 * kc * T::kTK * 2;
+      geo.b_bytes = p.Np * kc * T::kTK * 2;
+      geo.stage = (geo.a_bytes + geo.b_bytes + 1023) / 1024 * 1024;
+      geo.ring = (depth * (kc / 2) * T::kTileBytes + 127) / 128 * 128;
+      geo.ring_deep = depth;
+      geo.stages = (budget - dev::kTcDecodeWarps * geo.ring) / geo.stage;
+      if (geo.stages >= 3 && best.stages < 3) best = geo;
+      if (geo.stages > best.stages && best.stages < 3) best = geo;
+    }
   }
+  geo = best;
   if (geo.stages > 6) geo.stages = 6;
   if (geo.stages < 2) return cudaErrorInvalidConfiguration;
   geo.tmem_cols = 32;
   while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
-  const int smem = geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring + (3 * geo.stages + 1) * 8 + 16;
+  const int smem = geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring +
+                   (3 * geo.stages + 1 + dev::kTcDecodeWarps * geo.ring_deep) * 8 + 16;
   // split K over a cluster when the 128-row blocks alone leave SMs idle
   const int rb = (p.row_tiles + 7) / 8;
   int cs = 1;
@@ -487,10 +515,18 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   const int nchunks = p.Np / 16;
   const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
   if (cs > 1 && geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring < recv) cs = 1;
+  auto go = [&](auto cs_c) {
+    constexpr int C = decltype(cs_c)::value;
+    switch (geo.ring_deep) {
+      case 8: return launch_tc_m<SCHEME, C, 8>(p, geo, smem, rb, s);
+      case 4: return launch_tc_m<SCHEME, C, 4>(p, geo, smem, rb, s);
+      default: return launch_tc_m<SCHEME, C, 2>(p, geo, smem, rb, s);
+    }
+  };
   switch (cs) {
-    case 2: return launch_tc_m<SCHEME, 2>(p, geo, smem, rb, s);
-    case 4: return launch_tc_m<SCHEME, 4>(p, geo, smem, rb, s);
-    default: return launch_tc_m<SCHEME, 1>(p, geo, smem, rb, s);
+    case 2: return go(std::integral_constant<int, 2>{});
+    case 4: return go(std::integral_constant<int, 4>{});
+    default: return go(std::integral_constant<int, 1>{});
   }
 }
 

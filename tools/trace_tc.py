@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Per-CTA timeline of one K3 (tcgen05) launch: start, per-stage A ready (decode warp 0) and
+MMA commits, epilogue start/end (globaltimer, us from the first CTA start)."""
+import argparse, os, sys
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa
+import paper_2510_16045_b200 as amsq  # noqa
+from paper_2510_16045_b200._lib import lib  # noqa
+ap = argparse.ArgumentParser()
+ap.add_argument("--scheme", default="fp5.33-e2m3"); ap.add_argument("--n", type=int, default=4096)
+ap.add_argument("--k", type=int, default=4096); ap.add_argument("--m", type=int, default=32)
+a = ap.parse_args()
+sid = amsq.scheme_by_name(a.scheme).id
+ws = [amsq.DeviceWeight(bench.make_payload(sid, a.n, a.k, seed=c)) for c in range(3)]
+x = torch.randn(a.m, a.k, device="cuda").half(); y = torch.empty(a.m, a.n, device="cuda", dtype=torch.float16)
+tr = torch.zeros(1024 * 64, dtype=torch.int64, device="cuda")
+for i in range(6): ws[i % 3].linear(x, out=y)
+torch.cuda.synchronize()
+lib().amsq_debug_set_trace(tr.data_ptr()); ws[0].linear(x, out=y); torch.cuda.synchronize()
+lib().amsq_debug_set_trace(None)
+t = tr.view(1024, 64).cpu().numpy().astype(np.float64)
+n = int((t[:, 0] > 0).sum()); t = t[:n]; t0 = t[:, 0].min()
+r = lambda v: (v - t0) / 1e3
+print(f"{a.scheme} N={a.n} K={a.k} M={a.m}: ctas={n}")
+for name, i in (("start", 0), ("epilogue", 2), ("end", 3)):
+    v = r(t[:, i]); print(f"  {name:9s} min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}")
+for c in (0, n // 2):
+    a_ = [r(t[c, 8 + s]) for s in range(24) if t[c, 8 + s] > 0]
+    m_ = [r(t[c, 32 + s]) for s in range(24) if t[c, 32 + s] > 0]
+    print(f"  CTA {c}: A ready", " ".join(f"{v:.2f}" for v in a_))
+    print(f"  CTA {c}: MMA commit", " ".join(f"{v:.2f}" for v in m_))
