@@ -191,7 +191,14 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 constexpr int kConsumerWarps = AMSQ_K2_WARPS;
 constexpr bool kK2XPrep = AMSQ_K2_XPREP != 0;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
-constexpr int kMaxOwn = 4;                              // row tiles per consumer warp
+#ifndef AMSQ_MAX_OWN1  // row tiles a consumer warp may own at M <= 8 (4 or 8)
+#define AMSQ_MAX_OWN1 4
+#endif
+constexpr int kMaxOwn = 4;  // row tiles per consumer warp at M <= 16
+template <int NB>
+struct OwnCap {
+  static constexpr int value = NB == 1 ? AMSQ_MAX_OWN1 : kMaxOwn;
+};
 
 struct K2Geom {
   int S, wr;         // k-tiles per stage; warps sharing a k-slot (row-tile interleave)
@@ -284,15 +291,16 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   }
   __syncthreads();
 
-  float acc[kMaxOwn][NB][4];
+  constexpr int MAXOWN = OwnCap<NB>::value;
+  float acc[MAXOWN][NB][4];
 #pragma unroll
-  for (int i = 0; i < kMaxOwn; ++i)
+  for (int i = 0; i < MAXOWN; ++i)
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][nb][e] = 0.0f;
   const int ks = warp / geo.wr, rl = warp % geo.wr;  // k-slot (2 k-tiles per stage), row lane
-  const int nown = warp < kConsumerWarps && rl < G ? min(kMaxOwn, (G - rl + geo.wr - 1) / geo.wr) : 0;
+  const int nown = warp < kConsumerWarps && rl < G ? min(MAXOWN, (G - rl + geo.wr - 1) / geo.wr) : 0;
 
   // The CTA's K range [kb, ke) is walked from a per-group rotation rho: every CTA reads
   // the SAME activations, and all of them starting at k = 0 would hammer the same L2
@@ -500,6 +508,12 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
         case 2: consume(sp, nk, std::integral_constant<int, 2>{}); break;
         case 3: consume(sp, nk, std::integral_constant<int, 3>{}); break;
         case 4: consume(sp, nk, std::integral_constant<int, 4>{}); break;
+#if AMSQ_MAX_OWN1 > 4
+        case 5: if constexpr (MAXOWN >= 5) consume(sp, nk, std::integral_constant<int, 5>{}); break;
+        case 6: if constexpr (MAXOWN >= 6) consume(sp, nk, std::integral_constant<int, 6>{}); break;
+        case 7: if constexpr (MAXOWN >= 7) consume(sp, nk, std::integral_constant<int, 7>{}); break;
+        case 8: if constexpr (MAXOWN >= 8) consume(sp, nk, std::integral_constant<int, 8>{}); break;
+#endif
         default: break;
       }
       __syncwarp();
@@ -519,7 +533,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   const int items = G * 32 * NB4;
   if (warp < kConsumerWarps) {
 #pragma unroll
-    for (int i = 0; i < kMaxOwn; ++i) {
+    for (int i = 0; i < MAXOWN; ++i) {
       if (i < nown) {
         float* dst = red + (static_cast<long long>(ks) * G + rl + i * geo.wr) * 32 * NB4 + lane * NB4;
 #pragma unroll
@@ -613,15 +627,19 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const int G = p.plan.g_big;
   // wr: the smallest divisor of the consumer-warp count giving each warp <= 2 row tiles
   // (<= 4 when even all warps on one k-slot cannot)
+  const int own_target = NB == 1 ? (AMSQ_MAX_OWN1 > AMSQ_OWN_TARGET ? AMSQ_MAX_OWN1 : AMSQ_OWN_TARGET)
+                                  : AMSQ_OWN_TARGET;
   int wr = dev::kConsumerWarps;
   for (int d = 1; d <= dev::kConsumerWarps; ++d) {
-    if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= AMSQ_OWN_TARGET) {
+    if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= own_target) {
       wr = d;
       break;
     }
   }
   geo.wr = wr;
-  geo.kpw = NB == 2 ? 1 : 2;  // M <= 16 carries 2x the activation bytes per k-tile
+  // M <= 16 carries 2x the activation bytes per k-tile; > 4 row tiles per warp already makes
+  // a large stage
+  geo.kpw = (NB == 2 || (G + wr - 1) / wr > 4) ? 1 : 2;
   geo.S = geo.kpw * (dev::kConsumerWarps / wr);
   geo.w_stage = (geo.S * G * T::kTileBytes + 127) / 128 * 128;
   const int x_raw = geo.S * T::kTK * 2;
