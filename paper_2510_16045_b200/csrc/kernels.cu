@@ -273,6 +273,8 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   const int nst = ke > kb ? (ke - kb + S - 1) / S : 0;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
   uint64_t* empty = full + geo.stages;
+  // the group's row scales (fp32, x 2^14), staged once so the epilogue does not wait on HBM
+  float* sscale = reinterpret_cast<float*>(empty + geo.stages);
   unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
   if (trace && threadIdx.x == 0) {
     trace[0] = globaltimer();
@@ -288,6 +290,10 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < G * 16; i += blockDim.x) {
+    const long long n = static_cast<long long>(rt0) * 16 + i;
+    sscale[i] = n < p.rows ? __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale : 0.0f;
   }
   __syncthreads();
 
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     // runs of stage st: [k0, k0 + n0) then [k1, k1 + n1) (n1 = 0 when it does not wrap)
     auto runs = [&](int st, int& k0, int& n0, int& k1, int& n1) {
       const int q0 = st * S, nk = min(S, L - q0);
-      const int start = (rho + q0) % L;
+      const int start = rho + q0 >= L ? rho + q0 - L : rho + q0;  // rho, q0 < L: no division
       k0 = kb + start;
       n0 = min(nk, L - start);
       k1 = kb;
@@ -555,7 +561,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     const int m = nb * 8 + 2 * (ln & 3) + (e & 1);
     const long long n = static_cast<long long>(rt0 + r) * 16 + (ln >> 2) + 8 * (e >> 1);
     if (m < p.M && n < p.rows) {
-      const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
+      const float sc = sscale[n - static_cast<long long>(rt0) * 16];
       p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
     }
   };
@@ -648,13 +654,13 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   geo.xrows = (dev::kK2XPrep && NB == 2) ? 16 : p.M;
   const int x_stage = (dev::kK2XPrep && NB == 2) ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
   geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
-  const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024;
+  const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024 - G * 16 * 4;
   geo.stages = budget / geo.stage;
   if (geo.stages > 6) geo.stages = 6;
   // the epilogue reuses the ring: (S/kpw + csplit) x G x 32 x NB*4 floats
   const long long red = (static_cast<long long>(geo.S / geo.kpw) + p.plan.csplit) * G * 32 * NB * 4 * 4;
   while (geo.stages * geo.stage < red) ++geo.stages;
-  *smem_bytes = geo.stages * geo.stage + 2 * geo.stages * 8 + 16;
+  *smem_bytes = geo.stages * geo.stage + 2 * geo.stages * 8 + G * 16 * 4 + 16;
   return geo;
 }
 
