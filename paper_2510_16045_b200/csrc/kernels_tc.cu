@@ -4,13 +4,14 @@
 //
 // Swap-AB: D[128 weight rows][Np batch] += W[128 x K] . X^T[K x Np], D in TMEM (128 lanes x
 // Np fp32 columns), one CTA per 128-row block (8 row tiles of the tile layout).
-//  * warps 0..15 ("decode"): two per row tile (even / odd k-tiles of each stage); each
-//    streams its tiles from HBM through a private 4-deep cp.async ring, decodes in registers
-//    (the same decode_s4 / decode_s7 as K2) and stores the placed fp16 pairs into the stage's
-//    A buffer in the UMMA canonical K-major no-swizzle layout [k/8][128 rows][8];
-//    fence.proxy.async + one mbarrier arrival per warp.
-//  * warp 16 ("B producer"): one cp.async.bulk per stage of the activations, prepped once per
-//    call by amsq_xprep_tc_kernel into the same [k/8][Np][8] image; owns the TMEM allocation.
+//  * warps 0..15 ("decode"): two per row tile (even / odd k-tiles of each stage); each reads
+//    its tiles from the stage's weight buffer, decodes in registers (the same decode_s4 /
+//    decode_s7 as K2) and stores the placed fp16 pairs into the stage's A buffer in the UMMA
+//    canonical K-major no-swizzle layout [k/8][128 rows][8]; fence.proxy.async + one
+//    mbarrier arrival per warp.
+//  * warp 16 ("producer"): per stage, bulk copies of the block's weight tiles (one per row
+//    group segment, see below) and of the activation image (prepped once per call by
+//    amsq_xprep_tc_kernel into the same [k/8][Np][8] layout); owns the TMEM allocation.
 //  * warp 17 ("MMA"): one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
 //    N=Np, K=16) per 16 columns and tcgen05.commit's the stage back to the producers.
 //  * epilogue (warps 0..7): tcgen05.ld 32x32b -> fp32 * scale * 2^14 -> fp16 y; a cluster of
@@ -123,10 +124,8 @@ struct TcGeom {
   int stages;
   int a_bytes;  // A buffer per stage: 128 rows x kchunk*TK fp16
   int b_bytes;  // B buffer per stage: Np rows x kchunk*TK fp16
-  int stage;    // a_bytes + b_bytes (128-aligned)
+  int stage;    // A + activation image + weight tiles (8 row tiles x kchunk), 1 KB aligned
   int tmem_cols;
-  int ring;     // per decode warp: RING stages x kchunk/2 tiles (bytes, 128-aligned)
-  int ring_deep;  // ring depth in stages (8, 4 or 2: the deepest that fits)
 };
 
 __device__ __forceinline__ uint32_t tc_cluster_rank() {
@@ -141,9 +140,15 @@ __device__ __forceinline__ void tc_cluster_sync() {
 
 // CS CTAs of a cluster split K for one 128-row block; their TMEM partials are summed through
 // distributed shared memory (each 16-column chunk has an owner rank, round robin).
-template <int SCHEME, int CS, int RING>
+//
+// Weights reach shared memory through the producer's bulk copies: the block's 8 row tiles are
+// cut into segments by the layout's row groups (device_layout.hpp); a segment that is a whole
+// group is ONE copy per stage ([k_tile][row_tile] contiguous), a partial one is one copy per
+// k-tile. Few large copies keep the bulk engine's per-copy cost off the critical path.
+constexpr int kTcMaxSeg = 8;
+
+template <int SCHEME, int CS>
 __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams p, TcGeom geo) {
-  constexpr int kTcRing = RING;  // per-warp cp.async weight ring depth (stages)
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, TK = T::kTK, J = T::kJ;
   constexpr int RUN = SCHEME == 7 ? 12 : 16;  // columns a lane emits per row and tile
@@ -155,14 +160,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const int kper = (KT + CS - 1) / CS;
   const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
   const int nst = ke > kb ? (ke - kb + geo.kchunk - 1) / geo.kchunk : 0;
-  uint8_t* rings = smem + geo.stages * geo.stage;  // [kTcDecodeWarps][ring]
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(rings + kTcDecodeWarps * geo.ring);
-  uint64_t* fullB = fullA + geo.stages;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
+  uint64_t* fullB = fullA + geo.stages;  // activations + weights of the stage landed
   uint64_t* empty = fullB + geo.stages;
   uint64_t* done = empty + geo.stages;
-  uint64_t* rbar = done + 1;  // [kTcDecodeWarps][RING] weight-ring slot barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kTcDecodeWarps * RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  int* seg = reinterpret_cast<int*>(tmem_slot + 4);  // [kTcMaxSeg][4]: row0, rows, whole, src tile
   const uint32_t lboA = 128 * 16, lboB = static_cast<uint32_t>(p.Np) * 16;
+  const int rb0 = blk * 8, rb1 = min(rb0 + 8, p.row_tiles);
+  const GroupPlan& P = p.plan;
 
   unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
@@ -174,8 +180,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
-    for (int i = 0; i < kTcDecodeWarps * RING; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
+    // segments of the block by row group
+    int nseg = 0, r = rb0;
+    const int big_rows = P.n_big * P.g_big;
+    while (r < rb1 && nseg < kTcMaxSeg) {
+      const int g = r < big_rows ? r / P.g_big : P.n_big + (r - big_rows) / (P.g_big - 1);
+      const int g0 = P.row0(g), gs = P.size(g);
+      const int end = min(rb1, g0 + gs);
+      seg[nseg * 4 + 0] = r - rb0;
+      seg[nseg * 4 + 1] = end - r;
+      seg[nseg * 4 + 2] = (r == g0 && end == g0 + gs) ? gs : -gs;  // +G whole, -G partial
+      seg[nseg * 4 + 3] = g0 * KT + (r - g0);                     // tile index of (r, kt = 0)
+      ++nseg;
+      r = end;
+    }
+    for (int i = nseg; i < kTcMaxSeg; ++i) seg[i * 4 + 1] = 0;
   }
   if (warp == kTcDecodeWarps) {  // TMEM: Np fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -190,65 +210,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 
   if (warp < kTcDecodeWarps) {
     // ------------------------------------------------------------------ decode warps
-    // warp w: row tile 8*blk + (w & 7), the k-tiles of parity w >> 3 of every stage. Its
-    // tiles stream through a private kTcRing-deep cp.async ring (one commit group per stage)
-    // so ~kTcRing stages of weights are in flight per warp without holding registers.
-    const int rt = blk * 8 + (warp & 7), par = warp >> 3;
-    const bool live = rt < p.row_tiles;
+    // warp w: row tile rb0 + (w & 7), the k-tiles of parity w >> 3 of every stage
+    const int rtl = warp & 7, par = warp >> 3;
+    const bool live = rb0 + rtl < rb1;
     const int g = lane >> 2, t = lane & 3;
-    const GroupPlan& P = p.plan;
-    int G = 1, r0 = 0;
-    if (live) {
-      const int big_rows = P.n_big * P.g_big;
-      const int grp = rt < big_rows ? rt / P.g_big : P.n_big + (rt - big_rows) / (P.g_big - 1);
-      G = P.size(grp);
-      r0 = P.row0(grp);
-    }
-    // tile (rt, kt) lives at ((r0 * KT) + kt * G + (rt - r0)) * TILE (device_layout.hpp)
-    const uint8_t* tbase = p.w + (static_cast<long long>(r0) * KT + (rt - r0)) * TILE;
-    const long long kstride = static_cast<long long>(G) * TILE;
-    const int half_chunk = geo.kchunk / 2;
-    uint8_t* ring = rings + warp * geo.ring;
-    // slot refills go through the bulk engine (one copy per tile, completion on the slot's
-    // mbarrier): the per-stage fence.proxy.async below would otherwise wait for this
-    // thread's outstanding cp.async (LDGSTS) and serialise the ring
-    uint64_t* mybar = rbar + warp * kTcRing;
-    auto issue = [&](int st) {  // lane 0
-      if (st >= nst) return;
-      const int si = st % kTcRing;
-      uint8_t* slot = ring + si * half_chunk * TILE;
-      uint32_t bytes = 0;
-      for (int j = 0; j < half_chunk; ++j) {
-        const int kt = kb + st * geo.kchunk + 2 * j + par;
-        if (live && kt < ke) bytes += TILE;
+    // where this row tile sits in a stage's weight buffer: segment base + [kk][row in segment]
+    int wbase = 0, srows = 1, sr = 0;
+    for (int i = 0; i < kTcMaxSeg; ++i) {
+      const int r0 = seg[i * 4 + 0], n = seg[i * 4 + 1];
+      if (n == 0) break;
+      if (rtl >= r0 && rtl < r0 + n) {
+        srows = n;
+        sr = rtl - r0;
+        break;
       }
-      mbar_arrive_expect_tx(&mybar[si], bytes);
-      for (int j = 0; j < half_chunk; ++j) {
-        const int kt = kb + st * geo.kchunk + 2 * j + par;
-        if (live && kt < ke) {
-          bulk_g2s(slot + j * TILE, tbase + kt * kstride, TILE, &mybar[si], policy_evict_first());
-        }
-      }
-    };
-    if (lane == 0) {
-      for (int st = 0; st < kTcRing - 1; ++st) issue(st);
+      wbase += geo.kchunk * n * TILE;
     }
     int sidx = 0;
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
-      if (lane == 0) issue(st + kTcRing - 1);
-      mbar_wait(&mybar[st % kTcRing], (st / kTcRing) & 1);
-      if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
+      mbar_wait(&fullB[sidx], ph);  // this stage's weights (and activations) landed
+      if (st >= geo.stages) {
+        // A[sidx] is free once the MMAs of its previous use completed; fullB implies that
+        // the producer saw `empty` for this stage, so this wait returns at once
+        mbar_wait(&empty[sidx], ph ^ 1u);
+      }
       uint8_t* A = smem + sidx * geo.stage;
-      const uint8_t* slot = ring + (st % kTcRing) * half_chunk * TILE;
-      for (int j = 0; j < half_chunk; ++j) {
-        const int kk = 2 * j + par;
+      const uint8_t* W = A + geo.a_bytes + geo.b_bytes + wbase;
+      for (int kk = par; kk < geo.kchunk; kk += 2) {
         if (kb + st * geo.kchunk + kk < ke) {
           uint4 wv = make_uint4(0, 0, 0, 0);
           uint32_t sh = 0;
           if (live) {
-            wv = *reinterpret_cast<const uint4*>(slot + j * TILE + lane * 16);
-            if (SCHEME == 4) sh = slot[j * TILE + 512 + lane];
+            const uint8_t* tp = W + (kk * srows + sr) * TILE;
+            wv = *reinterpret_cast<const uint4*>(tp + lane * 16);
+            if (SCHEME == 4) sh = tp[512 + lane];
           }
           uint32_t Af[J][4];
           const uint32_t R[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -274,7 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           const int c0 = kk * TK + RUN * t;  // first (permuted) column of the run
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int r = (warp & 7) * 16 + g + 8 * h;
+            const int r = rtl * 16 + g + 8 * h;
             const uint32_t* v = h ? rowg8 : rowg;
             if constexpr (RUN == 16) {  // two whole 8-column core rows
               *reinterpret_cast<uint4*>(A + (c0 >> 3) * lboA + r * 16) = make_uint4(v[0], v[1], v[2], v[3]);
@@ -289,26 +285,54 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           }
         }
       }
+#ifndef AMSQ_TC_NOFENCE  // profiling variant only: drops the generic->async proxy fence
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sidx]);
       if (trace && warp == 0 && lane == 0 && st < 24) trace[8 + st] = globaltimer();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
   } else if (warp == kTcDecodeWarps) {
-    // ------------------------------------------------------------------ B producer
+    // ------------------------------------------------------------------ producer
+    // per stage: the block's weight segments + the activation image, one full barrier
     if (lane == 0) {
-      pdl_wait();  // the prepped activations come from the previous kernel
+      const uint64_t pol = policy_evict_first();
       int sidx = 0;
       uint32_t ph = 0;
+      bool waited = false;
       for (int st = 0; st < nst; ++st) {
         if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
         const int kt0 = kb + st * geo.kchunk, nk = min(geo.kchunk, ke - kt0);
-        const uint32_t bytes = static_cast<uint32_t>(nk * TK / 8) * lboB;
-        mbar_arrive_expect_tx(&fullB[sidx], bytes);
-        bulk_g2s(smem + sidx * geo.stage + geo.a_bytes,
-                 p.xk + static_cast<long long>(kt0) * TK * p.Np, bytes, &fullB[sidx],
-                 policy_evict_last());
+        const uint32_t xbytes = static_cast<uint32_t>(nk * TK / 8) * lboB;
+        uint32_t wbytes = 0;
+        for (int i = 0; i < kTcMaxSeg; ++i) wbytes += static_cast<uint32_t>(seg[i * 4 + 1] * nk * TILE);
+        uint8_t* sp = smem + sidx * geo.stage;
+        mbar_arrive_expect_tx(&fullB[sidx], xbytes + wbytes);
+        uint8_t* wdst = sp + geo.a_bytes + geo.b_bytes;
+        for (int i = 0; i < kTcMaxSeg; ++i) {
+          const int n = seg[i * 4 + 1];
+          if (n == 0) break;
+          const int gsz = seg[i * 4 + 2];
+          const long long t0 = seg[i * 4 + 3];
+          if (gsz > 0) {  // whole group: [k_tile][row_tile] contiguous
+            bulk_g2s(wdst, p.w + (t0 + static_cast<long long>(kt0) * gsz) * TILE,
+                     static_cast<uint32_t>(nk * n * TILE), &fullB[sidx], pol);
+          } else {  // partial group: one copy of n row tiles per k-tile (row stride -gsz)
+            for (int kk = 0; kk < nk; ++kk) {
+              bulk_g2s(wdst + kk * n * TILE,
+                       p.w + (t0 + static_cast<long long>(kt0 + kk) * (-gsz)) * TILE,
+                       static_cast<uint32_t>(n * TILE), &fullB[sidx], pol);
+            }
+          }
+          wdst += geo.kchunk * n * TILE;
+        }
+        if (!waited) {
+          pdl_wait();  // the prepped activations come from the previous kernel
+          waited = true;
+        }
+        bulk_g2s(sp + geo.a_bytes, p.xk + static_cast<long long>(kt0) * TK * p.Np, xbytes,
+                 &fullB[sidx], policy_evict_last());
         if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
       }
     }
@@ -426,12 +450,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 }  // namespace dev
 
 // ---------------------------------------------------------------- launchers
-template <int SCHEME, int CS, int RING>
+template <int SCHEME, int CS>
 static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int smem, int rb,
                                cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS, RING>,
+    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -454,7 +478,7 @@ static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int sm
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME, CS, RING>, p, geo);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_linear_tc_kernel<SCHEME, CS>, p, geo);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -483,28 +507,21 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   dev::TcGeom geo{}, best{};
   best.stages = 0;
   const int budget = 227 * 1024 - 2048;
-  // prefer a deep (8-stage) per-warp weight ring (it sets the bytes in flight per SM) and
-  // >= 3 A/B stages; otherwise the configuration with the most A/B stages
-  for (int depth : {8, 4, 2}) {
-    for (int kc : {2, 4}) {
-      geo.kchunk = kc;
-      geo.a_bytes = 128 * kc * T::kTK * 2;
-      geo.b_bytes = p.Np * kc * T::kTK * 2;
-      geo.stage = (geo.a_bytes + geo.b_bytes + 1023) / 1024 * 1024;
-      geo.ring = (depth * (kc / 2) * T::kTileBytes + 127) / 128 * 128;
-      geo.ring_deep = depth;
-      geo.stages = (budget - dev::kTcDecodeWarps * geo.ring) / geo.stage;
-      if (geo.stages >= 3 && best.stages < 3) best = geo;
-      if (geo.stages > best.stages && best.stages < 3) best = geo;
-    }
+  for (int kc : {4, 2}) {  // k-tiles per stage (even: two decode warps per row tile)
+    geo.kchunk = kc;
+    geo.a_bytes = 128 * kc * T::kTK * 2;
+    geo.b_bytes = p.Np * kc * T::kTK * 2;
+    geo.stage = (geo.a_bytes + geo.b_bytes + 8 * kc * T::kTileBytes + 1023) / 1024 * 1024;
+    geo.stages = budget / geo.stage;
+    if (geo.stages >= 4 || geo.stages > best.stages) best = geo;
+    if (geo.stages >= 4) break;
   }
   geo = best;
   if (geo.stages > 6) geo.stages = 6;
   if (geo.stages < 2) return cudaErrorInvalidConfiguration;
   geo.tmem_cols = 32;
   while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
-  const int smem = geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring +
-                   (3 * geo.stages + 1 + dev::kTcDecodeWarps * geo.ring_deep) * 8 + 16;
+  const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16 + dev::kTcMaxSeg * 16;
   // split K over a cluster when the 128-row blocks alone leave SMs idle
   const int rb = (p.row_tiles + 7) / 8;
   int cs = 1;
@@ -514,19 +531,11 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   }
   const int nchunks = p.Np / 16;
   const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
-  if (cs > 1 && geo.stages * geo.stage + dev::kTcDecodeWarps * geo.ring < recv) cs = 1;
-  auto go = [&](auto cs_c) {
-    constexpr int C = decltype(cs_c)::value;
-    switch (geo.ring_deep) {
-      case 8: return launch_tc_m<SCHEME, C, 8>(p, geo, smem, rb, s);
-      case 4: return launch_tc_m<SCHEME, C, 4>(p, geo, smem, rb, s);
-      default: return launch_tc_m<SCHEME, C, 2>(p, geo, smem, rb, s);
-    }
-  };
+  if (cs > 1 && geo.stages * geo.stage < recv) cs = 1;
   switch (cs) {
-    case 2: return go(std::integral_constant<int, 2>{});
-    case 4: return go(std::integral_constant<int, 4>{});
-    default: return go(std::integral_constant<int, 1>{});
+    case 2: return launch_tc_m<SCHEME, 2>(p, geo, smem, rb, s);
+    case 4: return launch_tc_m<SCHEME, 4>(p, geo, smem, rb, s);
+    default: return launch_tc_m<SCHEME, 1>(p, geo, smem, rb, s);
   }
 }
 
