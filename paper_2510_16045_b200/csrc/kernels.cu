@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #define AMSQ_TRACE_STAGES 0
 #endif
 #ifndef AMSQ_K2_MODE  // profiling variants only (tools/build_variants.sh): 1 = stream only,
-#define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode
+#define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode, 4 = consume without copies
 #endif
 constexpr int kConsumerWarps = AMSQ_K2_WARPS;
 constexpr bool kK2XPrep = AMSQ_K2_XPREP != 0;
@@ -208,6 +208,9 @@ struct K2Geom {
   int xrows;         // natural-layout activation rows held per stage (= M)
   int stage;         // bytes per stage (weights + activations), 128-aligned
   int stages;        // ring depth
+  int recv_off;      // byte offset of the cluster reduction's receive buffer
+  int recv_in_ring;  // 1: it overlaps the ring, so peers may only store after a cluster barrier
+  int bar_off;       // byte offset of the mbarriers (then the staged scales)
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
   const int S = geo.S;
   const int nst = ke > kb ? (ke - kb + S - 1) / S : 0;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.bar_off);
   uint64_t* empty = full + geo.stages;
   // the group's row scales (fp32, x 2^14), staged once so the epilogue does not wait on HBM
   float* sscale = reinterpret_cast<float*>(empty + geo.stages);
@@ -291,9 +294,14 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     }
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < G * 16; i += blockDim.x) {
+  // the group's row scales (G * 16 <= 1024 rows, <= 2 per thread): loaded now, parked in
+  // shared memory only after the K loop so the load latency never delays the first copies
+  float my_scale[2] = {0.0f, 0.0f};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = threadIdx.x + h * kK2Threads;
     const long long n = static_cast<long long>(rt0) * 16 + i;
-    sscale[i] = n < p.rows ? __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale : 0.0f;
+    if (i < G * 16 && n < p.rows) my_scale[h] = __half2float(__ushort_as_half(__ldg(p.scales + n))) * kPlaceScale;
   }
   __syncthreads();
 
@@ -305,7 +313,11 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][nb][e] = 0.0f;
-  const int ks = warp / geo.wr, rl = warp % geo.wr;  // k-slot (2 k-tiles per stage), row lane
+  // k-slot (kpw k-tiles per stage) and row lane of the warp. Warp w runs on SM sub-partition
+  // w % 4; numbering row lanes slowest spreads the lanes that own one extra row tile (when wr
+  // does not divide G) over the sub-partitions instead of stacking them on one.
+  const int nks = kConsumerWarps / geo.wr;
+  const int ks = warp % nks, rl = warp / nks;
   const int nown = warp < kConsumerWarps && rl < G ? min(MAXOWN, (G - rl + geo.wr - 1) / geo.wr) : 0;
 
   // The CTA's K range [kb, ke) is walked from a per-group rotation rho: every CTA reads
@@ -339,6 +351,10 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       return static_cast<uint32_t>(left <= 0 ? 0 : (left >= nr * TK ? nr * TK : left) * 2);
     };
     auto issue_w = [&](int st, int sidx) {  // lane 0
+#if AMSQ_K2_MODE == 4  // profiling variant: no copies (consumers run on whatever the ring holds)
+      mbar_arrive(&full[sidx]);
+      return;
+#endif
       int k0, n0, k1, n1;
       runs(st, k0, n0, k1, n1);
       uint8_t* sp = smem + sidx * geo.stage;
@@ -374,6 +390,11 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
 #endif
     };
     auto issue_x = [&](int st, int sidx) {  // whole warp; ends with arrival 2 of 2
+#if AMSQ_K2_MODE == 4
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[sidx]);
+      return;
+#endif
       int k0, n0, k1, n1;
       runs(st, k0, n0, k1, n1);
       uint8_t* xs = smem + sidx * geo.stage + geo.w_stage;
@@ -533,7 +554,17 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   }
 
   // ------------------------------------------------------------------ epilogue
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = threadIdx.x + h * kK2Threads;
+    if (i < G * 16) sscale[i] = my_scale[h];
+  }
   __syncthreads();  // every stage consumed: the ring is free for the reduction
+  if (CS > 1 && geo.recv_in_ring) {
+    // peers store their partials into this CTA's ring (recv below): announce that the ring is
+    // idle here, and wait for the peers' announcements before storing into theirs
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
   const int nslots = S / geo.kpw;               // k-slots (a warp covers kpw k-tiles of a stage)
   float* red = reinterpret_cast<float*>(smem);  // [nslots][G][32][NB4]
   const int items = G * 32 * NB4;
@@ -553,8 +584,9 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   pdl_wait();  // outputs may still be read by the previous kernel
   // clusters: recv[C][items] -- rank q's partial of the items rank r finalises lands in
   // rank r's recv[q] (remote stores), one cluster barrier, then rank r sums in rank order
-  float* recv = red + static_cast<long long>(nslots) * items;
   const int Gs = (G + CS - 1) / CS;  // row tiles each rank finalises
+  const int owned = Gs * 32 * NB4;   // items per rank
+  float* recv = reinterpret_cast<float*>(smem + geo.recv_off);  // [CS][owned]
   auto store_y = [&](int it, float v) {
     const int r = it / (32 * NB4), rem = it - r * 32 * NB4;
     const int ln = rem / NB4, q = rem - ln * NB4, nb = q >> 2, e = q & 3;
@@ -565,6 +597,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
     }
   };
+  if (CS > 1 && geo.recv_in_ring) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     float v = 0.0f;
     for (int k = 0; k < nslots; ++k) v += red[static_cast<long long>(k) * items + it];  // slot order
@@ -572,7 +605,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       store_y(it, v);
     } else {
       const uint32_t owner = static_cast<uint32_t>((it / (32 * NB4)) / Gs);
-      float* dst = recv + static_cast<long long>(crank) * items + it;
+      float* dst = recv + static_cast<long long>(crank) * owned + (it - static_cast<int>(owner) * owned);
       if (owner == crank) {
         *dst = v;
       } else {
@@ -589,7 +622,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
       float v = 0.0f;
 #pragma unroll
-      for (int r = 0; r < CS; ++r) v += recv[static_cast<long long>(r) * items + it];  // rank order
+      for (int r = 0; r < CS; ++r) v += recv[static_cast<long long>(r) * owned + (it - i0)];  // rank order
       store_y(it, v);
     }
   }
@@ -657,10 +690,24 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024 - G * 16 * 4;
   geo.stages = budget / geo.stage;
   if (geo.stages > 6) geo.stages = 6;
-  // the epilogue reuses the ring: (S/kpw + csplit) x G x 32 x NB*4 floats
-  const long long red = (static_cast<long long>(geo.S / geo.kpw) + p.plan.csplit) * G * 32 * NB * 4 * 4;
-  while (geo.stages * geo.stage < red) ++geo.stages;
-  *smem_bytes = geo.stages * geo.stage + 2 * geo.stages * 8 + G * 16 * 4 + 16;
+  // the epilogue reuses the ring for the k-slot partials: (S/kpw) x G x 32 x NB*4 floats. A
+  // cluster's receive buffer ([C][ceil(G/C) x 32 x NB*4] floats) goes after the ring when the
+  // leftover space holds it -- peers may then store as soon as they are done -- else into the
+  // ring behind the partials, fenced by an extra cluster barrier.
+  const long long red = static_cast<long long>(geo.S / geo.kpw) * G * 32 * NB * 4 * 4;
+  const int C = p.plan.csplit;
+  const long long recv = C > 1 ? static_cast<long long>(C) * ((G + C - 1) / C) * 32 * NB * 4 * 4 : 0;
+  if (recv > 0 && geo.stages * geo.stage + recv <= budget && geo.stages * geo.stage >= red) {
+    geo.recv_off = geo.stages * geo.stage;
+    geo.recv_in_ring = 0;
+  } else {
+    while (geo.stages * geo.stage < red + recv) ++geo.stages;
+    geo.recv_off = static_cast<int>(red);
+    geo.recv_in_ring = recv > 0 ? 1 : 0;
+  }
+  geo.bar_off = geo.recv_in_ring || recv == 0 ? geo.stages * geo.stage
+                                              : static_cast<int>((geo.recv_off + recv + 127) / 128 * 128);
+  *smem_bytes = geo.bar_off + 2 * geo.stages * 8 + G * 16 * 4 + 16;
   return geo;
 }
 

@@ -171,7 +171,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const GroupPlan& P = p.plan;
 
   unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
-  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+  // profiling trace (clock64 unless noted): [0] start (globaltimer) [1] start [2]/[3] epilogue /
+  // end (globaltimer); per stage st < 8: [8+] producer loop top [16+] producer issued [24+]
+  // decode warp 0 weights landed [32+] warp 0 A ready [40+] MMA operands ready [48+] MMAs issued
+  // [56+] decode warp 15 A ready
+  const bool tr8 = trace != nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer(), trace[1] = clock64();
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < geo.stages; ++s) {
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     uint32_t ph = 0;
     for (int st = 0; st < nst; ++st) {
       mbar_wait(&fullB[sidx], ph);  // this stage's weights (and activations) landed
+      if (tr8 && warp == 0 && lane == 0 && st < 8) trace[24 + st] = clock64();
       if (st >= geo.stages) {
         // A[sidx] is free once the MMAs of its previous use completed; fullB implies that
         // the producer saw `empty` for this stage, so this wait returns at once
@@ -290,19 +296,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sidx]);
-      if (trace && warp == 0 && lane == 0 && st < 24) trace[8 + st] = globaltimer();
+      if (tr8 && lane == 0 && st < 8 && (warp == 0 || warp == 15)) trace[(warp ? 56 : 32) + st] = clock64();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
   } else if (warp == kTcDecodeWarps) {
     // ------------------------------------------------------------------ producer
-    // per stage: the block's weight segments + the activation image, one full barrier
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int sidx = 0;
-      uint32_t ph = 0;
-      bool waited = false;
-      for (int st = 0; st < nst; ++st) {
-        if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
+    // per stage: the block's weight segments + the activation image, one full barrier. The
+    // whole warp walks the loop (lane 0 issues): lanes parked at a later barrier while lane 0
+    // runs alone would leave the warp diverged across barriers.
+    const uint64_t pol = policy_evict_first();
+    int sidx = 0;
+    uint32_t ph = 0;
+    for (int st = 0; st < nst; ++st) {
+      if (tr8 && lane == 0 && st < 8) trace[8 + st] = clock64();
+      if (st >= geo.stages) mbar_wait(&empty[sidx], ph ^ 1u);
+      if (st == 0) pdl_wait();  // the prepped activations come from the previous kernel
+      if (lane == 0) {
         const int kt0 = kb + st * geo.kchunk, nk = min(geo.kchunk, ke - kt0);
         const uint32_t xbytes = static_cast<uint32_t>(nk * TK / 8) * lboB;
         uint32_t wbytes = 0;
@@ -327,27 +336,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           }
           wdst += geo.kchunk * n * TILE;
         }
-        if (!waited) {
-          pdl_wait();  // the prepped activations come from the previous kernel
-          waited = true;
-        }
         bulk_g2s(sp + geo.a_bytes, p.xk + static_cast<long long>(kt0) * TK * p.Np, xbytes,
                  &fullB[sidx], policy_evict_last());
-        if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+        if (tr8 && st < 8) trace[16 + st] = clock64();
       }
+      __syncwarp();
+      if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
   } else {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4)                                      // D: f32
-                             | (static_cast<uint32_t>(p.Np >> 3) << 17)     // N
-                             | (static_cast<uint32_t>(128 >> 4) << 24);     // M
-      int sidx = 0;
-      uint32_t ph = 0;
-      for (int st = 0; st < nst; ++st) {
-        mbar_wait(&fullA[sidx], ph);
-        mbar_wait(&fullB[sidx], ph);
-        tc_fence_after();
+    // whole warp waits, one thread issues
+    const uint32_t idesc = (1u << 4)                                      // D: f32
+                           | (static_cast<uint32_t>(p.Np >> 3) << 17)     // N
+                           | (static_cast<uint32_t>(128 >> 4) << 24);     // M
+    int sidx = 0;
+    uint32_t ph = 0;
+    for (int st = 0; st < nst; ++st) {
+      mbar_wait(&fullA[sidx], ph);
+      mbar_wait(&fullB[sidx], ph);
+      tc_fence_after();
+      if (tr8 && lane == 0 && st < 8) trace[40 + st] = clock64();
+      if (lane == 0) {
         const int nk = min(geo.kchunk, ke - (kb + st * geo.kchunk));
         const uint32_t a0 = smem_u32(smem + sidx * geo.stage);
         const uint32_t b0 = a0 + geo.a_bytes;
@@ -357,11 +366,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           tc_mma_f16(tmem, ad, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
         }
         tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
-        if (trace && st < 24) trace[32 + st] = globaltimer();
-        if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+        if (tr8 && st < 8) trace[48 + st] = clock64();
       }
-      tc_commit(done);
+      __syncwarp();
+      if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
+    if (lane == 0) tc_commit(done);
+    __syncwarp();
   }
 
   // ------------------------------------------------------------------ epilogue

@@ -25,8 +25,11 @@ r = lambda v: (v - t0) / 1e3
 print(f"{a.scheme} N={a.n} K={a.k} M={a.m}: ctas={n}")
 for name, i in (("start", 0), ("epilogue", 2), ("end", 3)):
     v = r(t[:, i]); print(f"  {name:9s} min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}")
+us = lambda c, v: (v - t[c, 1]) / 1965.0  # clock64 cycles -> us at the max SM clock
+rows = (("producer loop top", 8), ("producer issued", 16), ("w0 landed", 24), ("w0 A ready", 32),
+        ("w15 A ready", 56), ("MMA ready", 40), ("MMA issued", 48))
 for c in (0, n // 2):
-    a_ = [r(t[c, 8 + s]) for s in range(24) if t[c, 8 + s] > 0]
-    m_ = [r(t[c, 32 + s]) for s in range(24) if t[c, 32 + s] > 0]
-    print(f"  CTA {c}: A ready", " ".join(f"{v:.2f}" for v in a_))
-    print(f"  CTA {c}: MMA commit", " ".join(f"{v:.2f}" for v in m_))
+    print(f"  CTA {c} (us from CTA start, clock64):")
+    for name, base in rows:
+        v = [us(c, t[c, base + s]) for s in range(8) if t[c, base + s] > 0]
+        print(f"    {name:18s}", " ".join(f"{x:6.2f}" for x in v))
