@@ -176,6 +176,15 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_K2_XPREP  // 1: M <= 16 reads activations pre-permuted by amsq_xprep_kernel (an extra
 #define AMSQ_K2_XPREP 1  // launch); 0: natural rows + PRMT like M <= 8 (measured slower)
 #endif
+#ifndef AMSQ_RECV_STEAL  // 1: a ring of >= 4 stages gives one up for an out-of-ring receive buffer
+#define AMSQ_RECV_STEAL 1
+#endif
+#ifndef AMSQ_KPW2_MIN_STAGES  // fewest ring stages for which a warp takes 2 k-tiles per stage
+#define AMSQ_KPW2_MIN_STAGES 3  // (M <= 16)
+#endif
+#ifndef AMSQ_KPW2_MIN_STAGES1  // (M <= 8)
+#define AMSQ_KPW2_MIN_STAGES1 1
+#endif
 #ifndef AMSQ_OWN_TARGET  // row tiles per consumer warp the stage geometry aims for (<= 4)
 #define AMSQ_OWN_TARGET 4
 #endif
@@ -293,15 +302,6 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
-  }
-  // the group's row scales (G * 16 <= 1024 rows, <= 2 per thread): loaded now, parked in
-  // shared memory only after the K loop so the load latency never delays the first copies
-  float my_scale[2] = {0.0f, 0.0f};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int i = threadIdx.x + h * kK2Threads;
-    const long long n = static_cast<long long>(rt0) * 16 + i;
-    if (i < G * 16 && n < p.rows) my_scale[h] = __half2float(__ushort_as_half(__ldg(p.scales + n))) * kPlaceScale;
   }
   __syncthreads();
 
@@ -440,6 +440,14 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       __syncwarp();  // the lanes' plain stores happen-before lane 0's release
       if (lane == 0) mbar_arrive(&full[sidx]);
     };
+    // the group's row scales (fp32, x 2^14) for the epilogue, staged after the last copy is
+    // issued: the consumers still have a ring's worth of stages to go, which hides the loads
+    auto stage_scales = [&]() {
+      for (int i = lane; i < G * 16; i += 32) {
+        const long long n = static_cast<long long>(rt0) * 16 + i;
+        sscale[i] = n < p.rows ? __half2float(__ushort_as_half(__ldg(p.scales + n))) * kPlaceScale : 0.0f;
+      }
+    };
     // weights of the first ring-full of stages are independent of the previous kernel:
     // request them before griddepcontrol.wait
     // stage 0's weights do not depend on the previous kernel: request them before
@@ -467,6 +475,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
 #endif
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
+    stage_scales();
   } else {
     // ------------------------------------------------------------------ consumers
     // the warp's kpw k-tiles x NOWN row tiles of a stage, branch-free for a fixed NOWN
@@ -554,11 +563,6 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   }
 
   // ------------------------------------------------------------------ epilogue
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int i = threadIdx.x + h * kK2Threads;
-    if (i < G * 16) sscale[i] = my_scale[h];
-  }
   __syncthreads();  // every stage consumed: the ring is free for the reduction
   if (CS > 1 && geo.recv_in_ring) {
     // peers store their partials into this CTA's ring (recv below): announce that the ring is
@@ -676,20 +680,27 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
     }
   }
   geo.wr = wr;
-  // M <= 16 carries 2x the activation bytes per k-tile; > 4 row tiles per warp already makes
-  // a large stage
-  geo.kpw = (NB == 2 || (G + wr - 1) / wr > 4) ? 1 : 2;
-  geo.S = geo.kpw * (dev::kConsumerWarps / wr);
-  geo.w_stage = (geo.S * G * T::kTileBytes + 127) / 128 * 128;
-  const int x_raw = geo.S * T::kTK * 2;
-  const int target = SCHEME == 7 ? 96 : 16;  // lanes' LDS hit distinct banks
-  geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
-  geo.xrows = (dev::kK2XPrep && NB == 2) ? 16 : p.M;
-  const int x_stage = (dev::kK2XPrep && NB == 2) ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
-  geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
+  // kpw k-tiles per warp and stage: 2 (B fragments and loop overhead amortised over twice the
+  // tiles) unless that leaves fewer than AMSQ_KPW2_MIN_STAGES ring stages (large G x S tiles,
+  // or M <= 16's double activation bytes), or a warp already owns > 4 row tiles
   const int budget = (AMSQ_CTAS_PER_SM > 1 ? 113 : 227) * 1024 - 1024 - G * 16 * 4;
-  geo.stages = budget / geo.stage;
-  if (geo.stages > 6) geo.stages = 6;
+  const int target = SCHEME == 7 ? 96 : 16;  // lanes' LDS hit distinct banks
+  auto shape = [&](int kpw) {
+    geo.kpw = kpw;
+    geo.S = kpw * (dev::kConsumerWarps / wr);
+    geo.w_stage = (geo.S * G * T::kTileBytes + 127) / 128 * 128;
+    const int x_raw = geo.S * T::kTK * 2;
+    geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
+    geo.xrows = (dev::kK2XPrep && NB == 2) ? 16 : p.M;
+    const int x_stage = (dev::kK2XPrep && NB == 2) ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
+    geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
+    geo.stages = budget / geo.stage;
+    if (geo.stages > 6) geo.stages = 6;
+  };
+  shape(2);
+  if ((G + wr - 1) / wr > 4 || geo.stages < (NB == 2 ? AMSQ_KPW2_MIN_STAGES : AMSQ_KPW2_MIN_STAGES1)) {
+    shape(1);
+  }
   // the epilogue reuses the ring for the k-slot partials: (S/kpw) x G x 32 x NB*4 floats. A
   // cluster's receive buffer ([C][ceil(G/C) x 32 x NB*4] floats) goes after the ring when the
   // leftover space holds it -- peers may then store as soon as they are done -- else into the
@@ -697,6 +708,9 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const long long red = static_cast<long long>(geo.S / geo.kpw) * G * 32 * NB * 4 * 4;
   const int C = p.plan.csplit;
   const long long recv = C > 1 ? static_cast<long long>(C) * ((G + C - 1) / C) * 32 * NB * 4 * 4 : 0;
+  if (AMSQ_RECV_STEAL && recv > 0 && geo.stages >= 4 && geo.stages * geo.stage + recv > budget) {
+    --geo.stages;  // give a ring stage to the receive buffer rather than fence it with a barrier
+  }
   if (recv > 0 && geo.stages * geo.stage + recv <= budget && geo.stages * geo.stage >= red) {
     geo.recv_off = geo.stages * geo.stage;
     geo.recv_in_ring = 0;
