@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #define AMSQ_RECV_STEAL 1
 #endif
 #ifndef AMSQ_KPW2_MIN_STAGES  // fewest ring stages for which a warp takes 2 k-tiles per stage
-#define AMSQ_KPW2_MIN_STAGES 3  // (M <= 16)
+#define AMSQ_KPW2_MIN_STAGES 2  // (M <= 16)
 #endif
 #ifndef AMSQ_KPW2_MIN_STAGES1  // (M <= 8)
 #define AMSQ_KPW2_MIN_STAGES1 1
