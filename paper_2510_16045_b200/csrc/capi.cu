@@ -114,6 +114,27 @@ struct DeviceGuard {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Device scratch of the synchronous host-buffer entry points (amsq_gemv_host): one grow-only
+// buffer per calling thread and device. Never freed -- a thread-exit cudaFree could run after
+// the driver has shut down -- so at most one (largest x + y) buffer per thread and device.
+uint8_t* host_call_scratch(int device, size_t bytes) {
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+  };
+  thread_local Buf bufs[16];
+  if (device < 0 || device >= 16) throw amsqb::InvalidArgument("device ordinal out of range");
+  Buf& b = bufs[device];
+  if (b.n < bytes) {
+    if (b.p) ck(cudaFree(b.p), "cudaFree(scratch)");
+    b.p = nullptr;
+    b.n = 0;
+    ck(cudaMalloc(&b.p, bytes), "cudaMalloc(scratch)");
+    b.n = bytes;
+  }
+  return static_cast<uint8_t*>(b.p);
+}
+
 amsqb::GroupPlan plan_of(const amsqb::DeviceLayout& L) {
   return amsqb::GroupPlan{L.n_groups, L.g_big, L.n_big, L.csplit};
 }
@@ -551,15 +572,15 @@ int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batc
     if (!x || !y) throw amsqb::InvalidArgument("gemv: null host buffer");
     DeviceGuard dg(h->device);
     cudaStream_t st = as_stream(stream);
-    void* dx = nullptr;
-    void* dy = nullptr;
-    ck(cudaMallocAsync(&dx, x_len * 2, st), "cudaMallocAsync(x)");
-    ck(cudaMallocAsync(&dy, batch * h->L.rows * 2, st), "cudaMallocAsync(y)");
+    // per-thread, per-device scratch for x and y, grown on demand and reused: the call is
+    // synchronous, so a thread's previous call has finished with it before the next starts
+    const size_t xb = (x_len * 2 + 255) / 256 * 256, yb = batch * h->L.rows * 2;
+    uint8_t* scratch = host_call_scratch(h->device, xb + yb);
+    void* dx = scratch;
+    void* dy = scratch + xb;
     ck(cudaMemcpyAsync(dx, x, x_len * 2, cudaMemcpyHostToDevice, st), "H2D x");
     linear_impl(h, static_cast<const uint16_t*>(dx), batch, static_cast<uint16_t*>(dy), h->L.rows, st);
-    ck(cudaMemcpyAsync(y, dy, batch * h->L.rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
-    ck(cudaFreeAsync(dx, st), "cudaFreeAsync");
-    ck(cudaFreeAsync(dy, st), "cudaFreeAsync");
+    ck(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st), "D2H y");
     ck(cudaStreamSynchronize(st), "gemv sync");
   });
 }
