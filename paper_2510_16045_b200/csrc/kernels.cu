@@ -3,10 +3,11 @@
 //  K1 amsq_restore_kernel   restore_block / restore_matrix(_half) over the tile layout
 //                           (kernels.hpp:55-133 of the reference), bit-exact.
 //  K2 amsq_linear_kernel    fused restore + linear for batch M <= 16 (kernels.hpp:151-187):
-//                           warp-specialised persistent CTA per SM (TMA-bulk producer warp,
-//                           8 decode/MMA consumer warps), stream-K over (256-row block x
-//                           k-tile) units, m16n8k16 tensor-core MMAs with fp32 accumulation,
-//                           deterministic split-K fix-up (fixed order, no float atomics).
+//                           one warp-specialised CTA per SM (TMA-bulk producer warp, 16
+//                           decode/MMA consumer warps) per row group of the weight's plan, or
+//                           a cluster of 2/4/8 CTAs splitting its K; m16n8k16 tensor-core MMAs
+//                           with fp32 accumulation; partials reduced in shared memory / DSMEM
+//                           in a fixed order (deterministic, no float atomics, no workspace).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
