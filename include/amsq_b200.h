@@ -168,7 +168,9 @@ int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t*
                    size_t ldy, void* stream);
 
 /* The reference call shape end to end: host x in, host y out (H2D, kernel, D2H on
- * `stream`, synchronous on return). x_len must equal batch*cols. */
+ * `stream`, synchronous on return). x_len must equal batch*cols. The device copies of x and
+ * y live in a grow-only scratch buffer per calling thread and device (reused across calls,
+ * never freed); pinned host buffers avoid a staging copy in the driver. */
 int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batch, uint16_t* y,
                    void* stream);
 
