@@ -394,6 +394,7 @@ def run_batch_sweep(args, shapes, dev, stream, cap):
                                        8, 5, stream, cap)
     del dense
     torch.cuda.empty_cache()
+    k3_min = lib().amsq_debug_set_k3_min_batch(0)  # the library's K2 / K3 dispatch threshold
     for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
         sid = amsq.scheme_by_name(scheme).id
         for i, (name, (n, k)) in enumerate(shapes.items()):
@@ -411,7 +412,8 @@ def run_batch_sweep(args, shapes, dev, stream, cap):
                 us = _graph_us(call, 2 * len(ws), 5, stream, cap)
                 flops = 2.0 * m * n * k
                 out.append({"scheme": scheme, "layer": name, "N": n, "K": k, "M": m,
-                            "kernel": "K2 mma.sync" if m <= 16 else "K3 tcgen05",
+                            "kernel": ("K3 tcgen05" if m >= k3_min else
+                                       "K2 mma.sync" if m <= 32 else "K2 mma.sync x%d" % -(-m // 32)),
                             "us": round(us, 2), "packed_GBps": round(pb / us / 1e3, 1),
                             "hbm_frac": round(algorithmic_bytes(pb, n, k, m) / us / 1e3 / peak, 3),
                             "TFLOPs": round(flops / us / 1e6, 1),

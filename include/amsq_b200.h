@@ -192,6 +192,10 @@ uint64_t amsq_kernel_launch_count(void);
  * each fused-linear CTA (0 start, 1 first stage landed, 2 stream done, 3 end, 4..7 the
  * producer's first issues, 8+2s / 9+2s stage s landed / consumed); NULL = off. */
 void amsq_debug_set_trace(void* d_buf);
+/* Dispatch knob: batches of >= rows run the tcgen05 kernel (K3), smaller ones the mma.sync
+ * kernel (K2) in 32-row chunks. rows <= 0 only queries; values below 17 clamp to 17. Returns
+ * the previous threshold (default 65, the measured crossover). Process-wide. */
+int amsq_debug_set_k3_min_batch(int rows);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,7 @@ SIGNATURES = {
     "amsq_tp_unshard": (_I, [_P, _SZ, _SZ, _SZ, _P, _P]),
     "amsq_kernel_launch_count": (C.c_uint64, []),
     "amsq_debug_set_trace": (None, [_P]),
+    "amsq_debug_set_k3_min_batch": (_I, [_I]),
 }
 
 _lib = None

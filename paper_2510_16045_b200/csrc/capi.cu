@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -23,13 +24,16 @@ struct amsq_weight_s {
   int device = 0;
   uint8_t* d_w = nullptr;
   unsigned short* d_scales = nullptr;
-  uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 16 batch rows)
+  uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 32 batch rows)
 };
 
 namespace {
 
 thread_local std::string g_error;
 unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
+// batches of at least this many rows run K3 (tcgen05); smaller ones run K2 in chunks of
+// linear_max_batch_per_launch() rows (measured crossover)
+std::atomic<int> g_k3_min_batch{65};
 
 struct CudaError : std::runtime_error {
   cudaError_t code;
@@ -165,7 +169,7 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   cudaStream_t st = as_stream(stream);
   ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");
   ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
-  ck(cudaMalloc(&h->d_xperm, h->L.k_tiles * 4 * 16 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
+  ck(cudaMalloc(&h->d_xperm, h->L.k_tiles * 4 * 32 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
   ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
   ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
   ck(cudaStreamSynchronize(st), "upload sync");  // host staging buffers die here
@@ -201,7 +205,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.k_tiles = static_cast<int>(h->L.k_tiles);
   p.plan = plan_of(h->L);
   p.trace = g_trace;
-  if (batch > static_cast<size_t>(amsqb::linear_max_batch_per_launch())) {
+  if (batch >= static_cast<size_t>(g_k3_min_batch.load(std::memory_order_relaxed))) {
     // K3: tcgen05 tiles, up to 256 batch rows per launch (weights streamed once per launch)
     // the activation image is stream-ordered scratch (cudaMallocAsync: capturable in CUDA
     // graphs, pooled, and private to this call -- no race between streams)
@@ -471,7 +475,7 @@ int amsq_weight_clone(amsq_weight_t h, void* stream, amsq_weight_t* out) {
     cudaStream_t st = as_stream(stream);
     ck(cudaMalloc(&c->d_w, h->L.bytes()), "cudaMalloc(weights)");
     ck(cudaMalloc(&c->d_scales, h->L.row_tiles * 16 * sizeof(unsigned short)), "cudaMalloc(scales)");
-    ck(cudaMalloc(&c->d_xperm, h->L.k_tiles * 4 * 16 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
+    ck(cudaMalloc(&c->d_xperm, h->L.k_tiles * 4 * 32 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
     ck(cudaMemcpyAsync(c->d_w, h->d_w, h->L.bytes(), cudaMemcpyDeviceToDevice, st), "D2D weights");
     ck(cudaMemcpyAsync(c->d_scales, h->d_scales, h->L.row_tiles * 16 * 2, cudaMemcpyDeviceToDevice, st),
        "D2D scales");
@@ -627,5 +631,11 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
 uint64_t amsq_kernel_launch_count(void) { return amsqb::kernel_launch_count(); }
 
 void amsq_debug_set_trace(void* d_buf) { g_trace = static_cast<unsigned long long*>(d_buf); }
+
+int amsq_debug_set_k3_min_batch(int rows) {
+  const int prev = g_k3_min_batch.load();
+  if (rows > 0) g_k3_min_batch.store(rows < 17 ? 17 : rows);
+  return prev;
+}
 
 }  // extern "C"

@@ -205,9 +205,15 @@ constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
 #define AMSQ_MAX_OWN1 4
 #endif
 constexpr int kMaxOwn = 4;  // row tiles per consumer warp at M <= 16
+#ifndef AMSQ_MAX_OWN4  // row tiles a consumer warp may own at M <= 32 (accumulators: 16 fp32 each)
+#define AMSQ_MAX_OWN4 2
+#endif
+#ifndef AMSQ_K2_MAX_BATCH  // batch rows per K2 launch: 16 (NB <= 2) or 32 (NB = 4 for 17..32)
+#define AMSQ_K2_MAX_BATCH 32
+#endif
 template <int NB>
 struct OwnCap {
-  static constexpr int value = NB == 1 ? AMSQ_MAX_OWN1 : kMaxOwn;
+  static constexpr int value = NB == 1 ? AMSQ_MAX_OWN1 : NB == 2 ? kMaxOwn : AMSQ_MAX_OWN4;
 };
 
 struct K2Geom {
@@ -240,7 +246,7 @@ __device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo,
   constexpr int J = T::kJ, MS = 8 * NB;
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    if constexpr (kK2XPrep && NB == 2) {
+    if constexpr (kK2XPrep && NB >= 2) {
       const uint2* xu = reinterpret_cast<const uint2*>(xs) + ((ks * J) * MS + nb * 8 + g) * 4 + t;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
@@ -272,7 +278,7 @@ template <int SCHEME, int NB, int CS>
 __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kernel(LinearParams p, K2Geom geo) {
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, J = T::kJ, TK = T::kTK, MS = 8 * NB, NB4 = NB * 4;
-  constexpr bool kXPrep = kK2XPrep && NB == 2;
+  constexpr bool kXPrep = kK2XPrep && NB >= 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -543,8 +549,8 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       switch (nown) {  // warp-uniform and fixed per warp
         case 1: consume(sp, nk, std::integral_constant<int, 1>{}); break;
         case 2: consume(sp, nk, std::integral_constant<int, 2>{}); break;
-        case 3: consume(sp, nk, std::integral_constant<int, 3>{}); break;
-        case 4: consume(sp, nk, std::integral_constant<int, 4>{}); break;
+        case 3: if constexpr (MAXOWN >= 3) consume(sp, nk, std::integral_constant<int, 3>{}); break;
+        case 4: if constexpr (MAXOWN >= 4) consume(sp, nk, std::integral_constant<int, 4>{}); break;
 #if AMSQ_MAX_OWN1 > 4
         case 5: if constexpr (MAXOWN >= 5) consume(sp, nk, std::integral_constant<int, 5>{}); break;
         case 6: if constexpr (MAXOWN >= 6) consume(sp, nk, std::integral_constant<int, 6>{}); break;
@@ -671,8 +677,9 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   const int G = p.plan.g_big;
   // wr: the smallest divisor of the consumer-warp count giving each warp <= 2 row tiles
   // (<= 4 when even all warps on one k-slot cannot)
-  const int own_target = NB == 1 ? (AMSQ_MAX_OWN1 > AMSQ_OWN_TARGET ? AMSQ_MAX_OWN1 : AMSQ_OWN_TARGET)
-                                  : AMSQ_OWN_TARGET;
+  const int own_target = NB == 1   ? (AMSQ_MAX_OWN1 > AMSQ_OWN_TARGET ? AMSQ_MAX_OWN1 : AMSQ_OWN_TARGET)
+                         : NB == 2 ? AMSQ_OWN_TARGET
+                                   : AMSQ_MAX_OWN4;
   int wr = dev::kConsumerWarps;
   for (int d = 1; d <= dev::kConsumerWarps; ++d) {
     if (dev::kConsumerWarps % d == 0 && (G + d - 1) / d <= own_target) {
@@ -692,14 +699,14 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
     geo.w_stage = (geo.S * G * T::kTileBytes + 127) / 128 * 128;
     const int x_raw = geo.S * T::kTK * 2;
     geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
-    geo.xrows = (dev::kK2XPrep && NB == 2) ? 16 : p.M;
-    const int x_stage = (dev::kK2XPrep && NB == 2) ? geo.S * T::kJ * 16 * 4 * 8 : geo.xrows * geo.x_row;
+    geo.xrows = (dev::kK2XPrep && NB >= 2) ? 8 * NB : p.M;
+    const int x_stage = (dev::kK2XPrep && NB >= 2) ? geo.S * T::kJ * 8 * NB * 4 * 8 : geo.xrows * geo.x_row;
     geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
     geo.stages = budget / geo.stage;
     if (geo.stages > 6) geo.stages = 6;
   };
   shape(2);
-  if ((G + wr - 1) / wr > 4 || geo.stages < (NB == 2 ? AMSQ_KPW2_MIN_STAGES : AMSQ_KPW2_MIN_STAGES1)) {
+  if ((G + wr - 1) / wr > dev::OwnCap<NB>::value || geo.stages < (NB >= 2 ? AMSQ_KPW2_MIN_STAGES : AMSQ_KPW2_MIN_STAGES1)) {
     shape(1);
   }
   // the epilogue reuses the ring for the k-slot partials: (S/kpw) x G x 32 x NB*4 floats. A
@@ -763,7 +770,7 @@ static cudaError_t launch_linear_m(const LinearParams& p, cudaStream_t s) {
 
 template <int SCHEME, int NB>
 static cudaError_t launch_linear_t(const LinearParams& p, cudaStream_t s) {
-  if constexpr (NB == 2 && dev::kK2XPrep) {
+  if constexpr (NB >= 2 && dev::kK2XPrep) {
     // activations first (PDL-chained: waits for whoever produced x, lets the linear start
     // streaming weights as soon as it is scheduled)
     const int MS = 8 * NB;
@@ -791,14 +798,28 @@ static cudaError_t launch_linear_t(const LinearParams& p, cudaStream_t s) {
   }
 }
 
-int linear_max_batch_per_launch() { return 16; }
+int linear_max_batch_per_launch() { return AMSQ_K2_MAX_BATCH; }
 
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {  // NOLINT
   if (p.plan.n_groups <= 0) return cudaSuccess;
-  if (p.scheme_id == 4) {
-    return p.M <= 8 ? launch_linear_t<4, 1>(p, s) : launch_linear_t<4, 2>(p, s);
+  if (p.M > 16 && p.plan.g_big > dev::kConsumerWarps * dev::OwnCap<4>::value) {
+    // groups too tall for the M <= 32 kernel's accumulators: two M <= 16 launches
+    LinearParams a = p, b = p;
+    a.M = 16;
+    b.M = p.M - 16;
+    b.x = p.x + 16 * p.ldx;
+    b.y = p.y + 16 * p.ldy;
+    const cudaError_t e = launch_linear(a, s);
+    return e != cudaSuccess ? e : launch_linear(b, s);
   }
-  return p.M <= 8 ? launch_linear_t<7, 1>(p, s) : launch_linear_t<7, 2>(p, s);
+  if (p.scheme_id == 4) {
+    if (p.M <= 8) return launch_linear_t<4, 1>(p, s);
+    if (p.M <= 16 || AMSQ_K2_MAX_BATCH <= 16) return launch_linear_t<4, 2>(p, s);
+    return launch_linear_t<4, 4>(p, s);
+  }
+  if (p.M <= 8) return launch_linear_t<7, 1>(p, s);
+  if (p.M <= 16 || AMSQ_K2_MAX_BATCH <= 16) return launch_linear_t<7, 2>(p, s);
+  return launch_linear_t<7, 4>(p, s);
 }
 
 // [P][batch][n] -> [batch][P*n]

@@ -186,11 +186,36 @@ def test_cpp_dropin_against_reference(cuda):
     assert "0 failure(s)" in r.stdout
 
 
+@pytest.fixture
+def force_k3():
+    """Route every batch > 16 to K3 (default: K2 in 32-row chunks below 65 rows)."""
+    from paper_2510_16045_b200._lib import lib
+    prev = lib().amsq_debug_set_k3_min_batch(17)
+    yield
+    lib().amsq_debug_set_k3_min_batch(prev)
+
+
+@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("shape", [(33, 200), (300, 1000), (1000, 4098), (80000, 64)])
+@pytest.mark.parametrize("batch", [17, 24, 31, 32, 40, 64])
+def test_linear_k2_batch_chunks(cuda, orc, sid, shape, batch):
+    """17 <= M < 65 runs K2 in 32-row chunks (M <= 32: the NB = 4 kernel; groups taller than
+    32 row tiles fall back to two M <= 16 launches)."""
+    rows, cols = shape
+    qt = quantized_gaussian(sid, rows, cols, seed=batch * 5 + rows)
+    x = gaussian_x(batch, cols, seed=batch + 13)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
 @pytest.mark.parametrize("sid", SCHEMES)
 @pytest.mark.parametrize("shape", [(128, 64), (300, 1000), (1000, 4098)])
 @pytest.mark.parametrize("batch", [24, 32, 64, 100, 256, 300])
-def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch):
-    """M > 16 runs K3 (tcgen05.mma + TMEM, up to 256 batch rows per launch)."""
+def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch, force_k3):
+    """K3 (tcgen05.mma + TMEM, up to 256 batch rows per launch), forced for every M > 16."""
     rows, cols = shape
     qt = quantized_gaussian(sid, rows, cols, seed=batch * 3 + rows)
     x = gaussian_x(batch, cols, seed=batch + 11)
@@ -204,7 +229,7 @@ def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch):
 
 @pytest.mark.parametrize("sid", SCHEMES)
 @pytest.mark.parametrize("batch", [17, 48, 112, 144, 200])
-def test_linear_tcgen05_cluster_split_odd_chunks(cuda, orc, sid, batch):
+def test_linear_tcgen05_cluster_split_odd_chunks(cuda, orc, sid, batch, force_k3):
     """K3 with a 2/4-CTA K split and a batch whose 16-column chunk count is odd."""
     rows, cols = 512, 2048 if sid == 4 else 2049
     qt = quantized_gaussian(sid, rows, cols, seed=batch)
