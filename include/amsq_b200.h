@@ -160,7 +160,10 @@ int amsq_restore_to_host(amsq_weight_t h, int what, void* host_out, size_t bytes
 
 /* gemv (kernels.hpp:151-187): y[b][r] = fp16(sum_i w_i s_r x_b,i), fp32 accumulation.
  * d_x is [batch][cols] fp16 (logical cols), d_y is [batch][rows] fp16.
- * batch >= 1 (check_gemv_shapes, kernels.hpp:137-143 -> AMSQ_EINVAL). */
+ * batch >= 1 (check_gemv_shapes, kernels.hpp:137-143 -> AMSQ_EINVAL).
+ * Batches of 9..64 rows stage their activations in a workspace owned by the handle: calls
+ * on one handle from different streams must not overlap in time (give each stream its own
+ * amsq_weight_clone(), which shares the weights). Same-stream calls are always safe. */
 int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream);
 
 /* Same with an explicit output row stride (elements) for writing into a wider buffer. */
