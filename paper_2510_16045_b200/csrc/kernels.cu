@@ -525,9 +525,9 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
               acc[i][0][j & 3] += __uint_as_float((A[j][0] ^ A[j][1] ^ A[j][2] ^ A[j][3] ^ B[0][j][0]) & 0x3F0F0F0Fu);
 #else
 #pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
+            for (int j = 0; j < J; ++j)  // k-step outer: consecutive MMAs hit different accumulators
 #pragma unroll
-              for (int j = 0; j < J; ++j) mma16816(acc[i][nb], A[j], B[nb][j][0], B[nb][j][1]);
+              for (int nb = 0; nb < NB; ++nb) mma16816(acc[i][nb], A[j], B[nb][j][0], B[nb][j][1]);
 #endif
           }
         }

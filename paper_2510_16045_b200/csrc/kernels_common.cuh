@@ -163,7 +163,9 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
 // D[16x8,f32] += A[16x16,f16,row] * B[16x8,f16,col]
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
-  asm volatile(
+  // not volatile: no side effects beyond its outputs, so ptxas may interleave independent
+  // MMAs (other accumulators) between dependent ones
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
