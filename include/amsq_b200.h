@@ -124,6 +124,10 @@ int amsq_weight_upload_rows(int scheme_id, size_t rows, size_t cols, size_t padd
 /* Container bytes -> device in one step (container.hpp:79-115 read_amsq + upload). */
 int amsq_weight_upload_container(const uint8_t* in, size_t in_bytes, size_t row0, size_t nrows,
                                  int device, void* stream, amsq_weight_t* out);
+/* The same from a container FILE: mmap'd read-only, validated (container.hpp:79-115), and
+ * only the pages of rows [row0, row0+nrows) are read by the repack (nrows = 0: to the end). */
+int amsq_weight_upload_file(const char* path, size_t row0, size_t nrows, int device,
+                            void* stream, amsq_weight_t* out);
 int amsq_weight_download(amsq_weight_t h, uint16_t* scales, size_t n_scales, uint16_t* payload,
                          size_t payload_words);
 /* A second, independent device copy of h (same device; a device-to-device copy of the tile
@@ -161,9 +165,8 @@ int amsq_restore_to_host(amsq_weight_t h, int what, void* host_out, size_t bytes
 /* gemv (kernels.hpp:151-187): y[b][r] = fp16(sum_i w_i s_r x_b,i), fp32 accumulation.
  * d_x is [batch][cols] fp16 (logical cols), d_y is [batch][rows] fp16.
  * batch >= 1 (check_gemv_shapes, kernels.hpp:137-143 -> AMSQ_EINVAL).
- * Batches of 9..64 rows stage their activations in a workspace owned by the handle: calls
- * on one handle from different streams must not overlap in time (give each stream its own
- * amsq_weight_clone(), which shares the weights). Same-stream calls are always safe. */
+ * Reentrant: batches of 9..64 rows stage their activations in a per-(handle, stream)
+ * workspace, so calls on one handle from different streams may overlap. */
 int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream);
 
 /* Same with an explicit output row stride (elements) for writing into a wider buffer. */
@@ -181,13 +184,29 @@ int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batc
  * `shard` holds rows [rank*N/P, (rank+1)*N/P). Computes the local [batch][N/P] output,
  * all-gathers it with ncclAllGather over `nccl_comm` (an ncclComm_t), and writes the
  * reference-layout [batch][N] result into d_y. d_scratch must hold
- * 2*batch*(N/P)*(P+1) bytes. */
+ * 2*batch*(N/P)*(P+1) bytes. With nranks == 1 and no communicator it is amsq_linear_ld. */
 int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint16_t* d_y,
                    void* d_scratch, size_t scratch_bytes, void* nccl_comm, int nranks,
                    void* stream);
+/* Single-process multi-GPU form (one process drives every GPU through
+ * ncclCommInitAll communicators): rank r's shard, activations, output, scratch, communicator
+ * and stream are element r of each array; the all-gathers are issued as one NCCL group. */
+int amsq_linear_tp_group(int nranks, const amsq_weight_t* shards, const uint16_t* const* d_x,
+                         size_t batch, uint16_t* const* d_y, void* const* d_scratch,
+                         size_t scratch_bytes, void* const* nccl_comms, void* const* streams);
 /* [P][batch][n] -> [batch][P*n] permutation used after the gather (exposed for tests). */
 int amsq_tp_unshard(const uint16_t* d_gathered, size_t nranks, size_t batch, size_t n_local,
                     uint16_t* d_y, void* stream);
+
+/* NCCL plumbing for hosts that do not own a communicator (the bench, the Python TP driver):
+ * a 128-byte ncclUniqueId made on one rank and shared out of band, then one ncclComm_t per
+ * rank (ncclCommInitRank), or all ranks' communicators of a single process
+ * (ncclCommInitAll over `devices`). The returned void* is an ncclComm_t. */
+int amsq_nccl_unique_id(void* id_out, size_t bytes);
+int amsq_nccl_comm_init_rank(const void* id, size_t bytes, int nranks, int rank, int device,
+                             void** comm);
+int amsq_nccl_comm_init_all(int ndev, const int* devices, void** comms);
+int amsq_nccl_comm_destroy(void* comm);
 
 /* Number of this library's kernels launched so far in this process (bench accounting). */
 uint64_t amsq_kernel_launch_count(void);

@@ -106,7 +106,10 @@ class DeviceTensor {
 
 // ---- the reference free functions, synchronous, host in / host out ------------------
 
-// kernels.hpp:151-153 gemv(qt, x, batch, threads).
+// kernels.hpp:151-153 gemv(qt, x, batch, threads). The reference call shape is stateless, so
+// this uploads (repacks + H2D) the weight on EVERY call before the kernel runs -- tens of ms
+// for an 8B gate_up. It exists so the reference's tests run unchanged; serving code uploads
+// once into a DeviceTensor and calls DeviceTensor::gemv / linear.
 template <class QT>
 std::vector<uint16_t> gemv(const QT& qt, std::span<const uint16_t> x, size_t batch,
                            int /*threads*/ = 1) {

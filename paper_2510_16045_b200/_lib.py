@@ -77,6 +77,7 @@ SIGNATURES = {
     "amsq_weight_upload_rows": (_I, [_I, _SZ, _SZ, _SZ, _U16P, _U16P, _SZ, _SZ, _SZ, _I, _P,
                                      C.POINTER(_P)]),
     "amsq_weight_upload_container": (_I, [_U8P, _SZ, _SZ, _SZ, _I, _P, C.POINTER(_P)]),
+    "amsq_weight_upload_file": (_I, [C.c_char_p, _SZ, _SZ, _I, _P, C.POINTER(_P)]),
     "amsq_weight_download": (_I, [_P, _U16P, _SZ, _U16P, _SZ]),
     "amsq_weight_clone": (_I, [_P, _P, C.POINTER(_P)]),
     "amsq_weight_free": (_I, [_P]),
@@ -89,7 +90,12 @@ SIGNATURES = {
     "amsq_linear_ld": (_I, [_P, _P, _SZ, _P, _SZ, _P]),
     "amsq_gemv_host": (_I, [_P, _U16P, _SZ, _SZ, _U16P, _P]),
     "amsq_linear_tp": (_I, [_P, _P, _SZ, _P, _P, _SZ, _P, _I, _P]),
+    "amsq_linear_tp_group": (_I, [_I, _P, _P, _SZ, _P, _P, _SZ, _P, _P]),
     "amsq_tp_unshard": (_I, [_P, _SZ, _SZ, _SZ, _P, _P]),
+    "amsq_nccl_unique_id": (_I, [_P, _SZ]),
+    "amsq_nccl_comm_init_rank": (_I, [_P, _SZ, _I, _I, _I, C.POINTER(_P)]),
+    "amsq_nccl_comm_init_all": (_I, [_I, _P, _P]),
+    "amsq_nccl_comm_destroy": (_I, [_P]),
     "amsq_kernel_launch_count": (C.c_uint64, []),
     "amsq_debug_set_trace": (None, [_P]),
     "amsq_debug_set_k3_min_batch": (_I, [_I]),

@@ -13,6 +13,7 @@ the GPU and raise :class:`NoDeviceError` when there is none. There is no CPU fal
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -230,10 +231,14 @@ def load_amsq(path: str) -> QuantizedTensor:
 
 
 # ------------------------------------------------------------------ device weights
-def _stream_ptr(stream) -> Optional[int]:
+def _stream_ptr(stream, device: Optional[int] = None) -> Optional[int]:
+    """The raw cudaStream_t: `stream` itself, or torch's current stream OF `device` (the
+    library switches to the weight's device, and a stream of another device cannot launch
+    there)."""
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        dev = torch.cuda.current_device() if device is None else device
+        return torch.cuda.current_stream(dev).cuda_stream
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
@@ -247,7 +252,7 @@ class DeviceWeight:
                  nrows: Optional[int] = None):
         self._h = C.c_void_p(None)
         nrows = qt.rows - row0 if nrows is None else nrows
-        st = _stream_ptr(stream) if _torch_cuda_ok() else None
+        st = _stream_ptr(stream, device) if _torch_cuda_ok() else None
         check(lib().amsq_weight_upload_rows(
             qt.scheme.id, qt.rows, qt.cols, qt.padded_cols,
             np.ascontiguousarray(qt.scales).ctypes.data,
@@ -267,6 +272,22 @@ class DeviceWeight:
         buf = np.frombuffer(data, np.uint8)
         check(lib().amsq_weight_upload_container(buf.ctypes.data, buf.size, row0, nrows, device,
                                                  None, C.byref(self._h)), "upload_container")
+        info = self.info()
+        self.scheme = scheme_by_id(info.scheme_id)
+        self.rows, self.cols, self.padded_cols = int(info.rows), int(info.cols), int(info.padded_cols)
+        self.device = device
+        self.device_bytes = int(info.device_bytes)
+        self.payload_bytes = int(info.payload_bytes)
+        return self
+
+    @classmethod
+    def from_file(cls, path: str, device: int = 0, row0: int = 0, nrows: int = 0):
+        """An AMSQ container file, mmap'd and uploaded (only rows [row0, row0+nrows) are
+        read; container.hpp:79-115 validation)."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p(None)
+        check(lib().amsq_weight_upload_file(os.fsencode(path), row0, nrows, device, None,
+                                            C.byref(self._h)), "upload_file")
         info = self.info()
         self.scheme = scheme_by_id(info.scheme_id)
         self.rows, self.cols, self.padded_cols = int(info.rows), int(info.cols), int(info.padded_cols)
@@ -299,7 +320,7 @@ class DeviceWeight:
         if out is None:
             out = torch.empty((self.rows, self.padded_cols), dtype=torch.float16,
                               device=f"cuda:{self.device}")
-        check(lib().amsq_restore_grid_f16(self._h, out.data_ptr(), _stream_ptr(stream)),
+        check(lib().amsq_restore_grid_f16(self._h, out.data_ptr(), _stream_ptr(stream, self.device)),
               "restore_grid")
         return out
 
@@ -308,7 +329,7 @@ class DeviceWeight:
         if out is None:
             out = torch.empty((self.rows, self.cols), dtype=torch.float32,
                               device=f"cuda:{self.device}")
-        check(lib().amsq_restore_f32(self._h, out.data_ptr(), _stream_ptr(stream)), "restore_f32")
+        check(lib().amsq_restore_f32(self._h, out.data_ptr(), _stream_ptr(stream, self.device)), "restore_f32")
         return out
 
     def restore_f16(self, out=None, stream=None):
@@ -316,7 +337,7 @@ class DeviceWeight:
         if out is None:
             out = torch.empty((self.rows, self.cols), dtype=torch.float16,
                               device=f"cuda:{self.device}")
-        check(lib().amsq_restore_f16(self._h, out.data_ptr(), _stream_ptr(stream)), "restore_f16")
+        check(lib().amsq_restore_f16(self._h, out.data_ptr(), _stream_ptr(stream, self.device)), "restore_f16")
         return out
 
     def linear(self, x, out=None, stream=None):
@@ -328,14 +349,14 @@ class DeviceWeight:
         if out is None:
             out = torch.empty((x.shape[0], self.rows), dtype=torch.float16, device=x.device)
         check(lib().amsq_linear(self._h, x.data_ptr(), x.shape[0], out.data_ptr(),
-                                _stream_ptr(stream)), "linear")
+                                _stream_ptr(stream, self.device)), "linear")
         return out
 
     def gemv_host(self, x: np.ndarray, batch: int, stream=None) -> np.ndarray:
         """Host fp16 bits in/out through amsq_gemv_host (H2D + kernel + D2H)."""
         x = np.ascontiguousarray(x, np.uint16).reshape(-1)
         y = np.zeros(batch * self.rows, np.uint16)
-        st = _stream_ptr(stream) if _torch_cuda_ok() else None
+        st = _stream_ptr(stream, self.device) if _torch_cuda_ok() else None
         check(lib().amsq_gemv_host(self._h, x.ctypes.data, x.size, batch, y.ctypes.data, st),
               "gemv")
         return y
@@ -344,7 +365,8 @@ class DeviceWeight:
         """An independent device copy (device-to-device; no host round trip)."""
         out = DeviceWeight.__new__(DeviceWeight)
         out._h = C.c_void_p(None)
-        check(lib().amsq_weight_clone(self._h, _stream_ptr(stream), C.byref(out._h)), "clone")
+        check(lib().amsq_weight_clone(self._h, _stream_ptr(stream, self.device), C.byref(out._h)),
+              "clone")
         for k in ("scheme", "rows", "cols", "padded_cols", "device", "device_bytes", "payload_bytes"):
             if hasattr(self, k):
                 setattr(out, k, getattr(self, k))

@@ -5,11 +5,16 @@
 // message. Device entry points never fall back to the CPU: without a device they
 // fail with AMSQ_ENODEV.
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -24,7 +29,11 @@ struct amsq_weight_s {
   int device = 0;
   uint8_t* d_w = nullptr;
   unsigned short* d_scales = nullptr;
-  uint2* d_xperm = nullptr;  // activations in B-fragment order (<= 32 batch rows)
+  // K2's activation workspace for batches of 9..64 rows (x in B-fragment order, <= 32 rows
+  // per launch): one buffer per stream that used this handle, so calls on different
+  // streams never share one; calls on one stream are ordered by the stream itself.
+  std::mutex ws_mu;
+  std::vector<std::pair<void*, uint2*>> ws;
 };
 
 namespace {
@@ -156,7 +165,9 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   if (pc != amsqb::padded_cols(s, cols)) throw amsqb::InvalidArgument("upload: padded_cols mismatch");
   const size_t wpr = amsqb::words_per_row(s, pc);
   if (words != rows * wpr) throw amsqb::InvalidArgument("upload: payload size mismatch");
-  if (nrows == 0 || row0 + nrows > rows) throw amsqb::InvalidArgument("upload: row range out of bounds");
+  if (nrows == 0 || row0 >= rows || nrows > rows - row0) {
+    throw amsqb::InvalidArgument("upload: row range out of bounds");
+  }
   require_device(device);
   DeviceGuard dg(device);
   auto h = std::make_unique<amsq_weight_s>();
@@ -169,7 +180,6 @@ amsq_weight_t upload_impl(int scheme_id, size_t rows, size_t cols, size_t pc,
   cudaStream_t st = as_stream(stream);
   ck(cudaMalloc(&h->d_w, tiles.size()), "cudaMalloc(weights)");
   ck(cudaMalloc(&h->d_scales, sc.size() * sizeof(unsigned short)), "cudaMalloc(scales)");
-  ck(cudaMalloc(&h->d_xperm, h->L.k_tiles * 4 * 32 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
   ck(cudaMemcpyAsync(h->d_w, tiles.data(), tiles.size(), cudaMemcpyHostToDevice, st), "H2D weights");
   ck(cudaMemcpyAsync(h->d_scales, sc.data(), sc.size() * 2, cudaMemcpyHostToDevice, st), "H2D scales");
   ck(cudaStreamSynchronize(st), "upload sync");  // host staging buffers die here
@@ -181,8 +191,29 @@ void free_impl(amsq_weight_t h) {
   DeviceGuard dg(h->device);
   cudaFree(h->d_w);
   cudaFree(h->d_scales);
-  cudaFree(h->d_xperm);
+  for (auto& e : h->ws) cudaFree(e.second);
   delete h;
+}
+
+// The stream's K2 activation workspace on h (created on first use). A stream that is being
+// captured into a CUDA graph and has none yet gets a stream-ordered allocation for this call
+// instead (cudaMalloc is not capturable); the caller frees *async_ws after the launches.
+uint2* k2_workspace(amsq_weight_t h, cudaStream_t st, void** async_ws) {
+  const size_t bytes = h->L.k_tiles * 4 * 32 * 4 * sizeof(uint2);
+  std::lock_guard<std::mutex> lk(h->ws_mu);
+  for (auto& e : h->ws) {
+    if (e.first == static_cast<void*>(st)) return e.second;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  ck(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+  if (cs != cudaStreamCaptureStatusNone) {
+    ck(cudaMallocAsync(async_ws, bytes, st), "cudaMallocAsync(xperm)");
+    return static_cast<uint2*>(*async_ws);
+  }
+  uint2* d = nullptr;
+  ck(cudaMalloc(&d, bytes), "cudaMalloc(xperm)");
+  h->ws.emplace_back(static_cast<void*>(st), d);
+  return d;
 }
 
 void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,
@@ -196,7 +227,6 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.scheme_id = h->L.scheme_id;
   p.w = h->d_w;
   p.scales = h->d_scales;
-  p.xperm = h->d_xperm;
   p.rows = static_cast<long long>(h->L.rows);
   p.cols = static_cast<long long>(h->L.cols);
   p.ldx = p.cols;
@@ -237,6 +267,8 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     return;
   }
   const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
+  void* async_ws = nullptr;
+  if (batch > 8) p.xperm = k2_workspace(h, st, &async_ws);
   for (size_t b0 = 0; b0 < batch; b0 += step) {
     const size_t mb = batch - b0 < step ? batch - b0 : step;
     p.x = reinterpret_cast<const unsigned short*>(d_x) + b0 * h->L.cols;
@@ -244,6 +276,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     p.M = static_cast<int>(mb);
     ck(amsqb::launch_linear(p, st), "amsq_linear_kernel launch");
   }
+  if (async_ws) ck(cudaFreeAsync(async_ws, st), "cudaFreeAsync(xperm)");
 }
 
 void restore_impl(amsq_weight_t h, uint16_t* grid, float* f32, uint16_t* f16, cudaStream_t st) {
@@ -263,6 +296,30 @@ void restore_impl(amsq_weight_t h, uint16_t* grid, float* f32, uint16_t* f16, cu
   p.f32_out = f32;
   p.f16_out = reinterpret_cast<unsigned short*>(f16);
   ck(amsqb::launch_restore(p, st), "amsq_restore_kernel launch");
+}
+
+// A parsed container (container.hpp:79-115) -> device. The container stores little-endian
+// u16 runs; on this (little-endian) host they are used in place when 2-byte aligned -- the
+// repack then reads only the requested rows straight from the caller's (or the mmap's)
+// bytes -- and decoded into a copy otherwise.
+amsq_weight_t upload_container_view(const amsqb::ContainerView& v, size_t row0, size_t nrows,
+                                    int device, void* stream) {
+  if (row0 >= v.rows) throw amsqb::InvalidArgument("upload_container: row0 out of bounds");
+  if (nrows == 0) nrows = v.rows - row0;
+  static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "container runs are little-endian");
+  const bool aligned = (reinterpret_cast<uintptr_t>(v.scales) % 2 == 0) &&
+                       (reinterpret_cast<uintptr_t>(v.payload) % 2 == 0);
+  if (aligned) {
+    return upload_impl(v.scheme_id, v.rows, v.cols, v.padded_cols,
+                       reinterpret_cast<const uint16_t*>(v.scales),
+                       reinterpret_cast<const uint16_t*>(v.payload), v.payload_words, row0, nrows,
+                       device, stream);
+  }
+  std::vector<uint16_t> scales(v.rows), payload(v.payload_words);
+  std::memcpy(scales.data(), v.scales, v.rows * 2);
+  std::memcpy(payload.data(), v.payload, v.payload_words * 2);
+  return upload_impl(v.scheme_id, v.rows, v.cols, v.padded_cols, scales.data(), payload.data(),
+                     payload.size(), row0, nrows, device, stream);
 }
 
 }  // namespace
@@ -431,17 +488,39 @@ int amsq_weight_upload_rows(int id, size_t rows, size_t cols, size_t pc, const u
   });
 }
 
+
+
 int amsq_weight_upload_container(const uint8_t* in, size_t n, size_t row0, size_t nrows,
                                  int device, void* stream, amsq_weight_t* out) {
   return guarded([&] {
     if (!out || !in) throw amsqb::InvalidArgument("null argument");
-    const auto v = amsqb::container_parse(in, n);
-    std::vector<uint16_t> scales(v.rows), payload(v.payload_words);
-    for (size_t i = 0; i < v.rows; ++i) scales[i] = static_cast<uint16_t>(v.scales[2 * i] | v.scales[2 * i + 1] << 8);
-    for (size_t i = 0; i < v.payload_words; ++i) payload[i] = static_cast<uint16_t>(v.payload[2 * i] | v.payload[2 * i + 1] << 8);
-    if (nrows == 0) nrows = v.rows - row0;
-    *out = upload_impl(v.scheme_id, v.rows, v.cols, v.padded_cols, scales.data(), payload.data(),
-                       payload.size(), row0, nrows, device, stream);
+    *out = upload_container_view(amsqb::container_parse(in, n), row0, nrows, device, stream);
+  });
+}
+
+int amsq_weight_upload_file(const char* path, size_t row0, size_t nrows, int device,
+                            void* stream, amsq_weight_t* out) {
+  return guarded([&] {
+    if (!out || !path) throw amsqb::InvalidArgument("null argument");
+    const int fd = ::open(path, O_RDONLY | O_CLOEXEC);
+    if (fd < 0) throw amsqb::Corrupt(std::string("cannot open container ") + path);
+    struct stat st {};
+    if (::fstat(fd, &st) != 0 || st.st_size <= 0) {
+      ::close(fd);
+      throw amsqb::Corrupt(std::string("cannot stat container ") + path);
+    }
+    const size_t n = static_cast<size_t>(st.st_size);
+    void* m = ::mmap(nullptr, n, PROT_READ, MAP_PRIVATE, fd, 0);
+    ::close(fd);
+    if (m == MAP_FAILED) throw amsqb::Corrupt(std::string("cannot map container ") + path);
+    ::madvise(m, n, MADV_SEQUENTIAL);
+    struct Unmap {
+      void* p;
+      size_t n;
+      ~Unmap() { ::munmap(p, n); }
+    } unmap{m, n};
+    *out = upload_container_view(amsqb::container_parse(static_cast<const uint8_t*>(m), n), row0,
+                                 nrows, device, stream);
   });
 }
 
@@ -475,7 +554,6 @@ int amsq_weight_clone(amsq_weight_t h, void* stream, amsq_weight_t* out) {
     cudaStream_t st = as_stream(stream);
     ck(cudaMalloc(&c->d_w, h->L.bytes()), "cudaMalloc(weights)");
     ck(cudaMalloc(&c->d_scales, h->L.row_tiles * 16 * sizeof(unsigned short)), "cudaMalloc(scales)");
-    ck(cudaMalloc(&c->d_xperm, h->L.k_tiles * 4 * 32 * 4 * sizeof(uint2)), "cudaMalloc(xperm)");
     ck(cudaMemcpyAsync(c->d_w, h->d_w, h->L.bytes(), cudaMemcpyDeviceToDevice, st), "D2D weights");
     ck(cudaMemcpyAsync(c->d_scales, h->d_scales, h->L.row_tiles * 16 * 2, cudaMemcpyDeviceToDevice, st),
        "D2D scales");
@@ -611,7 +689,7 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
     const size_t need = 2 * batch * n * (static_cast<size_t>(nranks) + 1);
     if (!d_scratch || scratch_bytes < need) throw amsqb::InvalidArgument("linear_tp: scratch too small");
     cudaStream_t st = as_stream(stream);
-    if (nranks == 1) {
+    if (nranks == 1 && !nccl_comm) {
       linear_impl(shard, d_x, batch, d_y, n, st);
       return;
     }
@@ -625,6 +703,95 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
     ck(amsqb::launch_unshard(gathered, nranks, static_cast<int>(batch), static_cast<int>(n),
                              reinterpret_cast<unsigned short*>(d_y), st),
        "unshard launch");
+  });
+}
+
+int amsq_linear_tp_group(int nranks, const amsq_weight_t* shards, const uint16_t* const* d_x,
+                         size_t batch, uint16_t* const* d_y, void* const* d_scratch,
+                         size_t scratch_bytes, void* const* nccl_comms, void* const* streams) {
+  return guarded([&] {
+    if (nranks < 1 || !shards || !d_x || !d_y || !d_scratch || !nccl_comms || !streams) {
+      throw amsqb::InvalidArgument("linear_tp_group: null argument");
+    }
+    const size_t n = shards[0] ? shards[0]->L.rows : 0;
+    for (int r = 0; r < nranks; ++r) {
+      check_handle(shards[r]);
+      if (shards[r]->L.rows != n) throw amsqb::InvalidArgument("linear_tp_group: unequal shards");
+      if (!nccl_comms[r]) throw amsqb::InvalidArgument("linear_tp_group: null communicator");
+      if (!d_scratch[r] || scratch_bytes < 2 * batch * n * (static_cast<size_t>(nranks) + 1)) {
+        throw amsqb::InvalidArgument("linear_tp_group: scratch too small");
+      }
+    }
+    // 1) every rank's fused linear on its own device/stream
+    for (int r = 0; r < nranks; ++r) {
+      linear_impl(shards[r], d_x[r], batch, static_cast<uint16_t*>(d_scratch[r]), n,
+                  as_stream(streams[r]));
+    }
+    // 2) one thread drives all communicators: the gathers must be one NCCL group
+    ncclResult_t res = ncclGroupStart();
+    for (int r = 0; r < nranks && res == ncclSuccess; ++r) {
+      DeviceGuard dg(shards[r]->device);
+      uint16_t* local = static_cast<uint16_t*>(d_scratch[r]);
+      res = ncclAllGather(local, local + batch * n, batch * n, ncclFloat16,
+                          static_cast<ncclComm_t>(nccl_comms[r]), as_stream(streams[r]));
+    }
+    const ncclResult_t end = ncclGroupEnd();
+    if (res == ncclSuccess) res = end;
+    if (res != ncclSuccess) throw NcclError(std::string("ncclAllGather (group): ") + ncclGetErrorString(res));
+    // 3) [P][batch][n] -> [batch][P*n] on every rank
+    for (int r = 0; r < nranks; ++r) {
+      DeviceGuard dg(shards[r]->device);
+      const uint16_t* gathered = static_cast<const uint16_t*>(d_scratch[r]) + batch * n;
+      ck(amsqb::launch_unshard(reinterpret_cast<const unsigned short*>(gathered), nranks,
+                               static_cast<int>(batch), static_cast<int>(n),
+                               reinterpret_cast<unsigned short*>(d_y[r]), as_stream(streams[r])),
+         "unshard launch");
+    }
+  });
+}
+
+int amsq_nccl_unique_id(void* id_out, size_t bytes) {
+  return guarded([&] {
+    if (!id_out || bytes < sizeof(ncclUniqueId)) throw amsqb::InvalidArgument("nccl_unique_id: buffer < 128 bytes");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int amsq_nccl_comm_init_rank(const void* id, size_t bytes, int nranks, int rank, int device,
+                             void** comm) {
+  return guarded([&] {
+    if (!id || bytes < sizeof(ncclUniqueId) || !comm) throw amsqb::InvalidArgument("nccl_comm_init_rank: bad argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw amsqb::InvalidArgument("nccl_comm_init_rank: bad rank");
+    require_device(device);
+    DeviceGuard dg(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&c, nranks, uid, rank);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    *comm = c;
+  });
+}
+
+int amsq_nccl_comm_init_all(int ndev, const int* devices, void** comms) {
+  return guarded([&] {
+    if (ndev < 1 || !devices || !comms) throw amsqb::InvalidArgument("nccl_comm_init_all: bad argument");
+    for (int i = 0; i < ndev; ++i) require_device(devices[i]);
+    std::vector<ncclComm_t> cs(static_cast<size_t>(ndev));
+    const ncclResult_t r = ncclCommInitAll(cs.data(), ndev, devices);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclCommInitAll: ") + ncclGetErrorString(r));
+    for (int i = 0; i < ndev; ++i) comms[i] = cs[static_cast<size_t>(i)];
+  });
+}
+
+int amsq_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (!comm) return;
+    const ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
+    if (r != ncclSuccess) throw NcclError(std::string("ncclCommDestroy: ") + ncclGetErrorString(r));
   });
 }
 

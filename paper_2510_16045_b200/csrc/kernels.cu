@@ -738,12 +738,10 @@ static cudaError_t launch_linear_m(const LinearParams& p, cudaStream_t s) {
   int smem = 0;
   const dev::K2Geom geo = k2_geometry<SCHEME, NB>(p, &smem);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  static int configured = 0;  // per template instance; attribute is per-function
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_kernel<SCHEME, NB, CS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = 227 * 1024;
+  static std::atomic<uint64_t> configured{0};  // per template instance, one bit per device
+  if (const cudaError_t e = opt_in_max_smem(dev::amsq_linear_kernel<SCHEME, NB, CS>, configured);
+      e != cudaSuccess) {
+    return e;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(p.plan.n_groups * CS));

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <vector_types.h>
 
@@ -57,6 +58,21 @@ struct TcParams {
   GroupPlan plan;
   unsigned long long* trace;  // profiling only: per-CTA globaltimer stamps (null = off)
 };
+
+// Opt a kernel into 227 KB of dynamic shared memory on the CURRENT device. The attribute is
+// per function and per device, so `done` keeps one bit per device ordinal; two first callers
+// racing both set it (idempotent), never neither.
+template <typename Kernel>
+cudaError_t opt_in_max_smem(Kernel* fn, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);
 cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,

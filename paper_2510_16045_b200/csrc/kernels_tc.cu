@@ -464,12 +464,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 template <int SCHEME, int CS>
 static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int smem, int rb,
                                cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dev::amsq_linear_tc_kernel<SCHEME, CS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  static std::atomic<uint64_t> configured{0};  // per template instance, one bit per device
+  if (const cudaError_t e = opt_in_max_smem(dev::amsq_linear_tc_kernel<SCHEME, CS>, configured);
+      e != cudaSuccess) {
+    return e;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(rb * CS));

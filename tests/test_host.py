@@ -288,6 +288,29 @@ def test_device_entry_points_fail_loudly_without_gpu():
     assert rc != 0
 
 
+def test_container_file_upload_validates_before_the_device(tmp_path):
+    """amsq_weight_upload_file: mmap + container.hpp:79-115 validation. Missing or corrupt
+    files are data errors (CorruptError = std::runtime_error) on any machine; a valid file
+    without a GPU fails loudly with NoDeviceError (no CPU fallback)."""
+    import torch
+    qt = random_payload(4, 20, 128)
+    good = tmp_path / "w.amsq"
+    good.write_bytes(amsq.write_amsq(qt))
+    with pytest.raises(amsq.CorruptError):
+        amsq.DeviceWeight.from_file(str(tmp_path / "missing.amsq"))
+    bad = tmp_path / "bad.amsq"
+    bad.write_bytes(b"AMSX" + good.read_bytes()[4:])
+    with pytest.raises(amsq.CorruptError):
+        amsq.DeviceWeight.from_file(str(bad))
+    trunc = tmp_path / "trunc.amsq"
+    trunc.write_bytes(good.read_bytes()[:-2])
+    with pytest.raises(amsq.CorruptError):
+        amsq.DeviceWeight.from_file(str(trunc))
+    if not torch.cuda.is_available():
+        with pytest.raises(amsq.NoDeviceError):
+            amsq.DeviceWeight.from_file(str(good))
+
+
 def test_cpp_dropin_without_gpu():
     """tests/cpp/dropin_test.cpp (reference headers + include/amsq_b200.hpp): without a
     GPU every device call raises std::runtime_error and shape errors invalid_argument."""

@@ -110,3 +110,82 @@ def test_tp_device_path_world1_and_unshard_kernel(cuda, orc):
     want = tp.unshard_host(gathered.cpu().numpy(), P, batch, rows // P)
     assert np.array_equal(out.cpu().numpy(), want)
     check_linear(out.cpu().numpy().view(np.uint16), yref, yabs)
+
+
+def _comm_init_all(ndev):
+    import ctypes as C
+    from paper_2510_16045_b200._lib import check, lib
+    devs = (C.c_int * ndev)(*range(ndev))
+    comms = (C.c_void_p * ndev)()
+    check(lib().amsq_nccl_comm_init_all(ndev, devs, comms), "nccl_comm_init_all")
+    return comms
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sid", [4, 7])
+def test_tp_nccl_single_process_all_gpus(cuda, orc, sid):
+    """one process, ncclCommInitAll over every visible GPU (1 on the
+    single-GPU box, where the all-gather is a 1-rank NCCL collective), amsq_linear_tp_group:
+    per-rank fused linear on its N-shard, grouped ncclAllGather, unshard. The gathered
+    [M][N] output on every rank must meet the bar against the full reference gemv."""
+    import ctypes as C
+    from helpers import check_linear, gaussian_x, random_payload
+    from paper_2510_16045_b200 import DeviceWeight
+    from paper_2510_16045_b200._lib import check, lib
+    P = torch.cuda.device_count()
+    rows, cols, batch = 1024 * P, 8192, 4
+    qt = random_payload(sid, rows, cols, seed=P)
+    x = gaussian_x(batch, cols, seed=2)
+    comms = _comm_init_all(P)
+    shards, xs, ys, scr, streams = [], [], [], [], []
+    need = 2 * batch * (rows // P) * (P + 1)
+    for r in range(P):
+        row0, n = tp.shard_range(rows, P, r)
+        shards.append(DeviceWeight(qt, device=r, row0=row0, nrows=n))
+        with torch.cuda.device(r):
+            xs.append(torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(f"cuda:{r}"))
+            ys.append(torch.empty(batch, rows, dtype=torch.float16, device=f"cuda:{r}"))
+            scr.append(torch.empty(need, dtype=torch.uint8, device=f"cuda:{r}"))
+            streams.append(torch.cuda.current_stream(r).cuda_stream)
+    arr = lambda vals: (C.c_void_p * P)(*vals)  # noqa: E731
+    check(lib().amsq_linear_tp_group(P, arr([s.handle for s in shards]),
+                                     arr([t.data_ptr() for t in xs]), batch,
+                                     arr([t.data_ptr() for t in ys]),
+                                     arr([t.data_ptr() for t in scr]), need, comms,
+                                     arr(streams)), "linear_tp_group")
+    for r in range(P):
+        torch.cuda.synchronize(r)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    for r in range(P):
+        check_linear(ys[r].cpu().numpy().view(np.uint16), yref, yabs)
+    for r in range(P):
+        lib().amsq_nccl_comm_destroy(comms[r])
+
+
+@pytest.mark.gpu
+def test_tp_nccl_rank_comm_and_linear_tp(cuda, orc):
+    """The per-process form the bench uses at N>1: amsq_nccl_unique_id +
+    amsq_nccl_comm_init_rank, then amsq_linear_tp (here world 1: a 1-rank ncclAllGather)."""
+    import ctypes as C
+    from helpers import check_linear, gaussian_x, random_payload
+    from paper_2510_16045_b200 import DeviceWeight
+    from paper_2510_16045_b200._lib import check, lib
+    uid = (C.c_uint8 * 128)()
+    check(lib().amsq_nccl_unique_id(uid, 128), "unique_id")
+    comm = C.c_void_p()
+    check(lib().amsq_nccl_comm_init_rank(uid, 128, 1, 0, 0, C.byref(comm)), "init_rank")
+    sid, rows, cols, batch = 7, 2048, 4096, 16
+    qt = random_payload(sid, rows, cols, seed=9)
+    x = gaussian_x(batch, cols, seed=1)
+    dw = DeviceWeight(qt)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = torch.empty(batch, rows, dtype=torch.float16, device=cuda)
+    need = 2 * batch * rows * 2
+    scr = torch.empty(need, dtype=torch.uint8, device=cuda)
+    check(lib().amsq_linear_tp(dw.handle, xt.data_ptr(), batch, y.data_ptr(), scr.data_ptr(),
+                               need, comm, 1, torch.cuda.current_stream().cuda_stream), "tp")
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y.cpu().numpy().view(np.uint16), yref, yabs)
+    check(lib().amsq_nccl_comm_destroy(comm), "destroy")
