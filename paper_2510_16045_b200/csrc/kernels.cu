@@ -310,7 +310,12 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     }
     fence_barrier_init();
   }
+  __syncwarp();  // reconverge warp 0 before the aligned CTA barrier
   __syncthreads();
+  // DSMEM rule: a peer's shared memory may only be written once that peer is known to be
+  // running. Arrive now (nothing to publish yet: relaxed) and wait right before the first
+  // remote store in the epilogue, by which time every peer has long arrived.
+  if constexpr (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   constexpr int MAXOWN = OwnCap<NB>::value;
   float acc[MAXOWN][NB][4];
@@ -570,7 +575,9 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   }
 
   // ------------------------------------------------------------------ epilogue
+  __syncwarp();
   __syncthreads();  // every stage consumed: the ring is free for the reduction
+  if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers started
   if (CS > 1 && geo.recv_in_ring) {
     // peers store their partials into this CTA's ring (recv below): announce that the ring is
     // idle here, and wait for the peers' announcements before storing into theirs
@@ -627,6 +634,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     }
   }
   if constexpr (CS > 1) {
+    __syncwarp();
     cluster_sync_all();  // every rank's partials have landed in their owners' recv
     const int i0 = min(G, static_cast<int>(crank) * Gs) * 32 * NB4;
     const int i1 = min(G, static_cast<int>(crank + 1) * Gs) * 32 * NB4;

@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     }
     for (int i = nseg; i < kTcMaxSeg; ++i) seg[i * 4 + 1] = 0;
   }
+  __syncwarp();  // reconverge warp 0 before the aligned barriers below
   if (warp == kTcDecodeWarps) {  // TMEM: Np fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   if constexpr (CS > 1) {
     // every rank's MMAs have finished reading its stage ring before any rank writes partials
     // into a peer's (reused) ring
+    __syncwarp();
     tc_fence_before();
     tc_cluster_sync();
     tc_fence_after();
@@ -431,6 +433,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     }
   }
   if constexpr (CS > 1) {
+    __syncwarp();
     tc_fence_before();
     tc_cluster_sync();  // all remote partials have landed
     if (warp < kTcEpiWarps) {
@@ -450,6 +453,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     }
   }
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (warp == kTcDecodeWarps) {

@@ -31,7 +31,7 @@ def main():
     args = ap.parse_args()
     sid = amsq.scheme_by_name(args.scheme).id
     copies = max(2, int(np.ceil(260e6 / amsq.packed_payload_bytes(sid, args.n, args.k))))
-    ws = [amsq.DeviceWeight(bench.make_payload(sid, args.n, args.k, seed=c)) for c in range(copies)]
+    ws = [amsq.DeviceWeight(bench._qt(args.scheme, args.n, args.k, seed=c)) for c in range(copies)]
     x = torch.randn(args.m, args.k, device="cuda").half()
     y = torch.empty(args.m, args.n, device="cuda", dtype=torch.float16)
     for i in range(args.iters):

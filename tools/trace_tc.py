@@ -12,7 +12,7 @@ ap.add_argument("--scheme", default="fp5.33-e2m3"); ap.add_argument("--n", type=
 ap.add_argument("--k", type=int, default=4096); ap.add_argument("--m", type=int, default=32)
 a = ap.parse_args()
 sid = amsq.scheme_by_name(a.scheme).id
-ws = [amsq.DeviceWeight(bench.make_payload(sid, a.n, a.k, seed=c)) for c in range(3)]
+ws = [amsq.DeviceWeight(bench._qt(a.scheme, a.n, a.k, seed=c)) for c in range(3)]
 x = torch.randn(a.m, a.k, device="cuda").half(); y = torch.empty(a.m, a.n, device="cuda", dtype=torch.float16)
 tr = torch.zeros(1024 * 64, dtype=torch.int64, device="cuda")
 for i in range(6): ws[i % 3].linear(x, out=y)
