@@ -173,6 +173,14 @@ int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_
 int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y,
                    size_t ldy, void* stream);
 
+/* Activation dtypes (the reference is fp16-only, half.hpp; bf16 is the north star's
+ * addition). bf16 rows are brought to fp16 exactly up to a per-row power of two, which the
+ * epilogue undoes before the single rounding of y to bf16. y has the activations' dtype.
+ * ldy = 0 means rows. */
+enum { AMSQ_DTYPE_F16 = 0, AMSQ_DTYPE_BF16 = 1 };
+int amsq_linear_ex(amsq_weight_t h, const void* d_x, int x_dtype, size_t batch, void* d_y,
+                   int y_dtype, size_t ldy, void* stream);
+
 /* The reference call shape end to end: host x in, host y out (H2D, kernel, D2H on
  * `stream`, synchronous on return). x_len must equal batch*cols. The device copies of x and
  * y live in a grow-only scratch buffer per calling thread and device (reused across calls,
@@ -194,6 +202,29 @@ int amsq_linear_tp(amsq_weight_t shard, const uint16_t* d_x, size_t batch, uint1
 int amsq_linear_tp_group(int nranks, const amsq_weight_t* shards, const uint16_t* const* d_x,
                          size_t batch, uint16_t* const* d_y, void* const* d_scratch,
                          size_t scratch_bytes, void* const* nccl_comms, void* const* streams);
+/* ---- fused column-parallel TP: no NCCL collective. Every rank owns a
+ * device segment (flag words + an output arena) that all ranks can store into -- peer access
+ * in one process, CUDA IPC across processes. amsq_linear_tp_fused computes the rank's shard
+ * and its epilogue stores every output element straight into EVERY rank's arena at
+ * [m][rank*n + j] (NVLink stores, overlapped with the other CTAs' math); a one-block flag
+ * barrier (system-scope release/acquire, epoch counters kept on the device so the call is
+ * CUDA-graph replayable) then guarantees, in stream order, that this rank's arena holds the
+ * whole [batch][N] output at byte offset y_offset. Callers must not overwrite an arena
+ * region a peer may still be reading (use distinct offsets per layer, like NCCL user
+ * buffers). A peer that never arrives fails the barrier after 2 s (amsq_tp_error). */
+typedef struct amsq_tp_s* amsq_tp_t;
+/* One process, every rank's view at once (out[r]); devices may repeat (virtual ranks). */
+int amsq_tp_create_local(int nranks, const int* devices, size_t arena_bytes, amsq_tp_t* out);
+/* Multi-process: create this rank's segment and its 64-byte cudaIpcMemHandle; exchange the
+ * handles out of band (nranks x 64 bytes, rank order) and attach. */
+int amsq_tp_segment_create(int nranks, int rank, int device, size_t arena_bytes,
+                           void* ipc_handle_out, amsq_tp_t* out);
+int amsq_tp_attach(amsq_tp_t tp, const void* ipc_handles);
+int amsq_tp_arena(amsq_tp_t tp, void** arena, size_t* bytes);
+int amsq_tp_error(amsq_tp_t tp, int* error);
+int amsq_tp_destroy(amsq_tp_t tp);
+int amsq_linear_tp_fused(amsq_weight_t shard, amsq_tp_t tp, const uint16_t* d_x, size_t batch,
+                         size_t y_offset, void* stream);
 /* [P][batch][n] -> [batch][P*n] permutation used after the gather (exposed for tests). */
 int amsq_tp_unshard(const uint16_t* d_gathered, size_t nranks, size_t batch, size_t n_local,
                     uint16_t* d_y, void* stream);

@@ -91,6 +91,12 @@ class DeviceTensor {
   void linear(const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream = nullptr) const {
     check(amsq_linear(h_, d_x, batch, d_y, stream), "amsq_linear");
   }
+  // bf16 activations and output (amsq_linear_ex; ldy = 0 means rows).
+  void linear_bf16(const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy = 0,
+                   void* stream = nullptr) const {
+    check(amsq_linear_ex(h_, d_x, AMSQ_DTYPE_BF16, batch, d_y, AMSQ_DTYPE_BF16, ldy, stream),
+          "amsq_linear_ex");
+  }
   // The reference payload words back (inverse repack: bit-exact).
   void download(std::vector<uint16_t>& scales, std::vector<uint16_t>& payload) const {
     const amsq_weight_info_t i = info();

@@ -60,6 +60,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         glob.glob(os.path.join(CSRC, "*.inl")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     objs = []
     log = []
+    jobs = []
     common = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
               "-I", nccl_inc, "--expt-relaxed-constexpr"]
     for src in _sources():
@@ -70,7 +71,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
         cmd = [nvcc()] + ARCH + common + ["-Xptxas", "-v", "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc()] + ARCH + common + ["-x", "cu", "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        jobs.append((src, cmd))
+    # translation units compile in parallel (the K2 instances are split one scheme per file)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: (j, subprocess.run(j[1], capture_output=True, text=True)),
+                              jobs))
+    for (src, cmd), r in results:
         log.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

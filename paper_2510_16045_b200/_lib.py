@@ -50,6 +50,8 @@ class WeightInfo(C.Structure):
                 ("g_big", C.c_int), ("n_big", C.c_int), ("csplit", C.c_int)]
 
 
+AMSQ_DTYPE_F16, AMSQ_DTYPE_BF16 = 0, 1
+
 # Every symbol include/amsq_b200.h declares, with (restype, argtypes).
 _P, _SZ, _I, _U16P, _U8P = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p
 SIGNATURES = {
@@ -88,9 +90,17 @@ SIGNATURES = {
     "amsq_restore_to_host": (_I, [_P, _I, _P, _SZ, _P]),
     "amsq_linear": (_I, [_P, _P, _SZ, _P, _P]),
     "amsq_linear_ld": (_I, [_P, _P, _SZ, _P, _SZ, _P]),
+    "amsq_linear_ex": (_I, [_P, _P, _I, _SZ, _P, _I, _SZ, _P]),
     "amsq_gemv_host": (_I, [_P, _U16P, _SZ, _SZ, _U16P, _P]),
     "amsq_linear_tp": (_I, [_P, _P, _SZ, _P, _P, _SZ, _P, _I, _P]),
     "amsq_linear_tp_group": (_I, [_I, _P, _P, _SZ, _P, _P, _SZ, _P, _P]),
+    "amsq_tp_create_local": (_I, [_I, _P, _SZ, _P]),
+    "amsq_tp_segment_create": (_I, [_I, _I, _I, _SZ, _P, C.POINTER(_P)]),
+    "amsq_tp_attach": (_I, [_P, _P]),
+    "amsq_tp_arena": (_I, [_P, C.POINTER(_P), C.POINTER(_SZ)]),
+    "amsq_tp_error": (_I, [_P, C.POINTER(C.c_int)]),
+    "amsq_tp_destroy": (_I, [_P]),
+    "amsq_linear_tp_fused": (_I, [_P, _P, _P, _SZ, _SZ, _P]),
     "amsq_tp_unshard": (_I, [_P, _SZ, _SZ, _SZ, _P, _P]),
     "amsq_nccl_unique_id": (_I, [_P, _SZ]),
     "amsq_nccl_comm_init_rank": (_I, [_P, _SZ, _I, _I, _I, C.POINTER(_P)]),
@@ -112,6 +122,8 @@ def lib() -> C.CDLL:
                               "or `python -m paper_2510_16045_b200._build`")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if "AMSQ_LIB" in os.environ and not hasattr(L, name):
+                continue  # an older build loaded for A/B timing
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

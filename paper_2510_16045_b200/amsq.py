@@ -341,15 +341,25 @@ class DeviceWeight:
         return out
 
     def linear(self, x, out=None, stream=None):
-        """y[M][rows] = x[M][cols] @ W^T (fp16 in/out, fp32 accumulation)."""
+        """y[M][rows] = x[M][cols] @ W^T, fp32 accumulation; x and y fp16 (the reference's
+        dtype) or bf16 (amsq_linear_ex: exact power-of-two staging through fp16)."""
         import torch
-        if x.dim() != 2 or x.shape[1] != self.cols or x.dtype != torch.float16:
+        if x.dim() != 2 or x.shape[1] != self.cols or x.dtype not in (torch.float16,
+                                                                      torch.bfloat16):
             raise ValueError("gemv: activation shape mismatch")
         x = x.contiguous()
         if out is None:
-            out = torch.empty((x.shape[0], self.rows), dtype=torch.float16, device=x.device)
-        check(lib().amsq_linear(self._h, x.data_ptr(), x.shape[0], out.data_ptr(),
-                                _stream_ptr(stream, self.device)), "linear")
+            out = torch.empty((x.shape[0], self.rows), dtype=x.dtype, device=x.device)
+        elif out.dtype != x.dtype:
+            raise ValueError("linear: out dtype must match x")
+        st = _stream_ptr(stream, self.device)
+        if x.dtype == torch.float16:
+            check(lib().amsq_linear(self._h, x.data_ptr(), x.shape[0], out.data_ptr(), st),
+                  "linear")
+        else:
+            check(lib().amsq_linear_ex(self._h, x.data_ptr(), _lib.AMSQ_DTYPE_BF16, x.shape[0],
+                                       out.data_ptr(), _lib.AMSQ_DTYPE_BF16, out.stride(0), st),
+                  "linear")
         return out
 
     def gemv_host(self, x: np.ndarray, batch: int, stream=None) -> np.ndarray:

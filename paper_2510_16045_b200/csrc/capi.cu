@@ -36,7 +36,22 @@ struct amsq_weight_s {
   std::vector<std::pair<void*, uint2*>> ws;
 };
 
+// One rank's view of a fused-TP group (amsq_linear_tp_fused). Each rank owns a segment of
+// device memory [flags: nranks u32 | epoch u32 | error u32 | arena]; every rank can store into
+// every segment (peer access in one process, CUDA IPC across processes).
+struct amsq_tp_s {
+  int nranks = 0, rank = 0, device = 0;
+  uint8_t* seg = nullptr;          // this rank's segment (owned)
+  size_t arena_bytes = 0;
+  std::vector<uint8_t*> peer_seg;  // every rank's segment as seen from this device
+  std::vector<uint8_t*> opened;    // IPC-opened peer segments (to close)
+  unsigned short** d_y = nullptr;  // device array [nranks]: peers' arena bases
+  unsigned int** d_flags = nullptr;
+};
+
 namespace {
+
+constexpr size_t kTpHeader = 512;  // flags at 0, epoch at 256, error at 260, arena at 512
 
 thread_local std::string g_error;
 unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
@@ -216,11 +231,17 @@ uint2* k2_workspace(amsq_weight_t h, cudaStream_t st, void** async_ws) {
   return d;
 }
 
+struct TpArgs {
+  int nranks;
+  unsigned short* const* d_y;  // peers' output bases (already offset)
+  long long col0;
+};
+
 void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,
-                 cudaStream_t st) {
+                 cudaStream_t st, const float* yscale = nullptr, const TpArgs* tp = nullptr) {
   check_handle(h);
   if (batch == 0) throw amsqb::InvalidArgument("gemv: activation shape mismatch");
-  if (!d_x || !d_y) throw amsqb::InvalidArgument("linear: null device buffer");
+  if (!d_x || (!d_y && !tp)) throw amsqb::InvalidArgument("linear: null device buffer");
   if (ldy < h->L.rows) throw amsqb::InvalidArgument("linear: ldy < rows");
   DeviceGuard dg(h->device);
   amsqb::LinearParams p{};
@@ -235,7 +256,13 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.k_tiles = static_cast<int>(h->L.k_tiles);
   p.plan = plan_of(h->L);
   p.trace = g_trace;
-  if (batch >= static_cast<size_t>(g_k3_min_batch.load(std::memory_order_relaxed))) {
+  if (tp) {
+    p.tp_ranks = tp->nranks;
+    p.tp_y = tp->d_y;
+    p.tp_col0 = tp->col0;
+  }
+  const bool k3_scheme = h->L.scheme_id == 4 || h->L.scheme_id == 7;  // K3: the two AMS schemes
+  if (!tp && k3_scheme && batch >= static_cast<size_t>(g_k3_min_batch.load(std::memory_order_relaxed))) {
     // K3: tcgen05 tiles, up to 256 batch rows per launch (weights streamed once per launch)
     // the activation image is stream-ordered scratch (cudaMallocAsync: capturable in CUDA
     // graphs, pooled, and private to this call -- no race between streams)
@@ -255,6 +282,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     q.plan = p.plan;
     q.trace = g_trace;
     for (size_t b0 = 0; b0 < batch; b0 += amsqb::kTcMaxBatch) {
+      q.yscale = yscale ? yscale + b0 : nullptr;
       const size_t mb = batch - b0 < static_cast<size_t>(amsqb::kTcMaxBatch) ? batch - b0 : amsqb::kTcMaxBatch;
       q.M = static_cast<int>(mb);
       q.Np = static_cast<int>((mb + 15) / 16 * 16);
@@ -273,6 +301,8 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     const size_t mb = batch - b0 < step ? batch - b0 : step;
     p.x = reinterpret_cast<const unsigned short*>(d_x) + b0 * h->L.cols;
     p.y = reinterpret_cast<unsigned short*>(d_y) + b0 * ldy;
+    p.yscale = yscale ? yscale + b0 : nullptr;
+    if (tp) p.tp_col0 = tp->col0 + static_cast<long long>(b0 * ldy);
     p.M = static_cast<int>(mb);
     ck(amsqb::launch_linear(p, st), "amsq_linear_kernel launch");
   }
@@ -644,6 +674,37 @@ int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t*
   return guarded([&] { linear_impl(h, d_x, batch, d_y, ldy, as_stream(stream)); });
 }
 
+int amsq_linear_ex(amsq_weight_t h, const void* d_x, int x_dtype, size_t batch, void* d_y,
+                   int y_dtype, size_t ldy, void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    if (x_dtype != y_dtype || (x_dtype != AMSQ_DTYPE_F16 && x_dtype != AMSQ_DTYPE_BF16)) {
+      throw amsqb::InvalidArgument("linear_ex: supported dtypes are f16->f16 and bf16->bf16");
+    }
+    if (ldy == 0) ldy = h->L.rows;
+    cudaStream_t st = as_stream(stream);
+    if (x_dtype == AMSQ_DTYPE_F16) {
+      linear_impl(h, static_cast<const uint16_t*>(d_x), batch, static_cast<uint16_t*>(d_y), ldy, st);
+      return;
+    }
+    if (batch == 0) throw amsqb::InvalidArgument("gemv: activation shape mismatch");
+    if (!d_x || !d_y) throw amsqb::InvalidArgument("linear: null device buffer");
+    DeviceGuard dg(h->device);
+    // stream-ordered scratch (pooled; capturable): x as scaled fp16 + the per-row scales
+    const size_t xb = (batch * h->L.cols * 2 + 255) / 256 * 256;
+    void* ws = nullptr;
+    ck(cudaMallocAsync(&ws, xb + batch * sizeof(float), st), "cudaMallocAsync(bf16 prep)");
+    auto* xh = static_cast<unsigned short*>(ws);
+    auto* ys = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + xb);
+    ck(amsqb::launch_x_bf16_prep(static_cast<const unsigned short*>(d_x),
+                                 static_cast<long long>(h->L.cols), static_cast<long long>(h->L.cols),
+                                 static_cast<int>(batch), xh, ys, st),
+       "amsq_x_bf16_prep launch");
+    linear_impl(h, reinterpret_cast<const uint16_t*>(xh), batch, static_cast<uint16_t*>(d_y), ldy, st, ys);
+    ck(cudaFreeAsync(ws, st), "cudaFreeAsync(bf16 prep)");
+  });
+}
+
 int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batch, uint16_t* y,
                    void* stream) {
   return guarded([&] {
@@ -747,6 +808,158 @@ int amsq_linear_tp_group(int nranks, const amsq_weight_t* shards, const uint16_t
                                reinterpret_cast<unsigned short*>(d_y[r]), as_stream(streams[r])),
          "unshard launch");
     }
+  });
+}
+
+namespace {
+uint8_t* tp_segment_alloc(int device, int nranks, size_t arena_bytes) {
+  if (nranks < 1 || nranks > 64) throw amsqb::InvalidArgument("tp: 1 <= nranks <= 64");
+  require_device(device);
+  DeviceGuard dg(device);
+  uint8_t* seg = nullptr;
+  ck(cudaMalloc(&seg, kTpHeader + arena_bytes), "cudaMalloc(tp segment)");
+  ck(cudaMemset(seg, 0, kTpHeader + arena_bytes), "memset(tp segment)");
+  return seg;
+}
+
+// device arrays of the peers' arena bases and flag arrays, on the rank's device
+void tp_publish(amsq_tp_s* t) {
+  DeviceGuard dg(t->device);
+  std::vector<unsigned short*> y(static_cast<size_t>(t->nranks));
+  std::vector<unsigned int*> f(static_cast<size_t>(t->nranks));
+  for (int r = 0; r < t->nranks; ++r) {
+    y[static_cast<size_t>(r)] = reinterpret_cast<unsigned short*>(t->peer_seg[static_cast<size_t>(r)] + kTpHeader);
+    f[static_cast<size_t>(r)] = reinterpret_cast<unsigned int*>(t->peer_seg[static_cast<size_t>(r)]);
+  }
+  ck(cudaMalloc(&t->d_y, y.size() * sizeof(void*)), "cudaMalloc(tp ptrs)");
+  ck(cudaMalloc(&t->d_flags, f.size() * sizeof(void*)), "cudaMalloc(tp ptrs)");
+  ck(cudaMemcpy(t->d_y, y.data(), y.size() * sizeof(void*), cudaMemcpyHostToDevice), "H2D tp ptrs");
+  ck(cudaMemcpy(t->d_flags, f.data(), f.size() * sizeof(void*), cudaMemcpyHostToDevice), "H2D tp ptrs");
+}
+
+void tp_free(amsq_tp_s* t) {
+  if (!t) return;
+  DeviceGuard dg(t->device);
+  for (uint8_t* p : t->opened) cudaIpcCloseMemHandle(p);
+  cudaFree(t->d_y);
+  cudaFree(t->d_flags);
+  cudaFree(t->seg);
+  delete t;
+}
+}  // namespace
+
+int amsq_tp_create_local(int nranks, const int* devices, size_t arena_bytes, amsq_tp_t* out) {
+  return guarded([&] {
+    if (!devices || !out) throw amsqb::InvalidArgument("tp_create_local: null argument");
+    std::vector<std::unique_ptr<amsq_tp_s, void (*)(amsq_tp_s*)>> ts;
+    for (int r = 0; r < nranks; ++r) {
+      ts.emplace_back(new amsq_tp_s, tp_free);
+      amsq_tp_s* t = ts.back().get();
+      t->nranks = nranks, t->rank = r, t->device = devices[r], t->arena_bytes = arena_bytes;
+      t->seg = tp_segment_alloc(devices[r], nranks, arena_bytes);
+    }
+    for (int r = 0; r < nranks; ++r) {  // NVLink peer access between distinct devices
+      for (int q = 0; q < nranks; ++q) {
+        if (devices[r] == devices[q]) continue;
+        int ok = 0;
+        ck(cudaDeviceCanAccessPeer(&ok, devices[r], devices[q]), "cudaDeviceCanAccessPeer");
+        if (!ok) throw NoDevice("tp_create_local: no peer access between the GPUs");
+        DeviceGuard dg(devices[r]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+        } else {
+          ck(e, "cudaDeviceEnablePeerAccess");
+        }
+      }
+    }
+    for (auto& t : ts) {
+      for (auto& q : ts) t->peer_seg.push_back(q->seg);
+      tp_publish(t.get());
+    }
+    for (int r = 0; r < nranks; ++r) out[r] = ts[static_cast<size_t>(r)].release();
+  });
+}
+
+int amsq_tp_segment_create(int nranks, int rank, int device, size_t arena_bytes,
+                           void* ipc_handle_out, amsq_tp_t* out) {
+  return guarded([&] {
+    if (!ipc_handle_out || !out) throw amsqb::InvalidArgument("tp_segment_create: null argument");
+    if (rank < 0 || rank >= nranks) throw amsqb::InvalidArgument("tp_segment_create: bad rank");
+    std::unique_ptr<amsq_tp_s, void (*)(amsq_tp_s*)> t(new amsq_tp_s, tp_free);
+    t->nranks = nranks, t->rank = rank, t->device = device, t->arena_bytes = arena_bytes;
+    t->seg = tp_segment_alloc(device, nranks, arena_bytes);
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t hnd;
+    ck(cudaIpcGetMemHandle(&hnd, t->seg), "cudaIpcGetMemHandle");
+    std::memcpy(ipc_handle_out, &hnd, sizeof(hnd));
+    *out = t.release();
+  });
+}
+
+int amsq_tp_attach(amsq_tp_t t, const void* ipc_handles) {
+  return guarded([&] {
+    if (!t || !ipc_handles) throw amsqb::InvalidArgument("tp_attach: null argument");
+    if (!t->peer_seg.empty()) throw amsqb::InvalidArgument("tp_attach: already attached");
+    DeviceGuard dg(t->device);
+    const auto* hs = static_cast<const cudaIpcMemHandle_t*>(ipc_handles);
+    for (int r = 0; r < t->nranks; ++r) {
+      if (r == t->rank) {
+        t->peer_seg.push_back(t->seg);
+        continue;
+      }
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      t->opened.push_back(static_cast<uint8_t*>(p));
+      t->peer_seg.push_back(static_cast<uint8_t*>(p));
+    }
+    tp_publish(t);
+  });
+}
+
+int amsq_tp_arena(amsq_tp_t t, void** arena, size_t* bytes) {
+  return guarded([&] {
+    if (!t || !arena) throw amsqb::InvalidArgument("tp_arena: null argument");
+    *arena = t->seg + kTpHeader;
+    if (bytes) *bytes = t->arena_bytes;
+  });
+}
+
+int amsq_tp_destroy(amsq_tp_t t) {
+  return guarded([&] { tp_free(t); });
+}
+
+int amsq_linear_tp_fused(amsq_weight_t shard, amsq_tp_t t, const uint16_t* d_x, size_t batch,
+                         size_t y_offset, void* stream) {
+  return guarded([&] {
+    check_handle(shard);
+    if (!t || t->peer_seg.empty()) throw amsqb::InvalidArgument("linear_tp_fused: group not attached");
+    if (shard->device != t->device) throw amsqb::InvalidArgument("linear_tp_fused: shard on another device");
+    const size_t n = shard->L.rows, N = n * static_cast<size_t>(t->nranks);
+    if (y_offset % 2 || y_offset + 2 * batch * N > t->arena_bytes) {
+      throw amsqb::InvalidArgument("linear_tp_fused: output does not fit the arena");
+    }
+    DeviceGuard dg(t->device);
+    cudaStream_t st = as_stream(stream);
+    // peers' output bases at y_offset (a small device array per call shape, cached per handle
+    // would be an optimisation; the offset is folded into tp_col0 instead)
+    TpArgs tp{t->nranks, t->d_y, static_cast<long long>(y_offset / 2) +
+                                     static_cast<long long>(t->rank) * static_cast<long long>(n)};
+    linear_impl(shard, d_x, batch, nullptr, N, st, nullptr, &tp);
+    unsigned int* flags = reinterpret_cast<unsigned int*>(t->seg);
+    ck(amsqb::launch_tp_barrier(t->d_flags, flags, flags + 64, flags + 65, t->rank, t->nranks,
+                                2000000000ull, st),
+       "amsq_tp_barrier_kernel launch");
+  });
+}
+
+int amsq_tp_error(amsq_tp_t t, int* error) {
+  return guarded([&] {
+    if (!t || !error) throw amsqb::InvalidArgument("tp_error: null argument");
+    DeviceGuard dg(t->device);
+    unsigned int e = 0;
+    ck(cudaMemcpy(&e, t->seg + 260, 4, cudaMemcpyDeviceToHost), "D2H tp error");
+    *error = static_cast<int>(e);
   });
 }
 

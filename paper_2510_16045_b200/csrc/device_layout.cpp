@@ -16,13 +16,18 @@
 
 namespace amsqb {
 
-bool device_scheme_supported(int id) { return id == 4 || id == 7; }
+bool device_scheme_supported(int id) { return id >= 0 && id < kNumSchemes; }
+
+namespace {
+// (TK, tile bytes) per scheme: exactly the reference bits of a 16 x TK tile
+constexpr int kTileTK[8] = {64, 64, 64, 64, 64, 48, 64, 48};
+constexpr int kTileBytes[8] = {512, 640, 768, 768, 544, 416, 576, 512};
+}  // namespace
 
 DeviceLayout make_device_layout(int id, size_t rows, size_t cols, size_t pc) {
   const Scheme& s = scheme(id);
   if (!device_scheme_supported(id)) {
-    throw InvalidArgument(std::string("device layout: scheme ") + s.name +
-                          " has no sm_100a kernel (supported: fp4.25-e2m2, fp5.33-e2m3)");
+    throw InvalidArgument(std::string("device layout: scheme ") + s.name + " has no sm_100a kernel");
   }
   if (rows == 0 || cols == 0) throw InvalidArgument("device layout: empty tensor");
   if (pc != padded_cols(s, cols)) throw InvalidArgument("device layout: padded_cols mismatch");
@@ -30,8 +35,8 @@ DeviceLayout make_device_layout(int id, size_t rows, size_t cols, size_t pc) {
   L.scheme_id = id;
   L.rows = rows, L.cols = cols, L.padded_cols = pc;
   L.wpr = words_per_row(s, pc);
-  L.tk = id == 4 ? 64 : 48;
-  L.tile_bytes = id == 4 ? 544 : 512;
+  L.tk = static_cast<size_t>(kTileTK[id]);
+  L.tile_bytes = static_cast<size_t>(kTileBytes[id]);
   L.row_tiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   L.k_tiles = (pc + L.tk - 1) / L.tk;
   choose_plan(L.row_tiles, L.k_tiles, &L);
@@ -227,6 +232,187 @@ void s7_unpack_tile(const DeviceLayout& L, const uint8_t* tile, size_t rt, size_
   }
 }
 
+// ---------------------------------------------------------------- the nibble family
+// Schemes 0, 1, 2, 3, 5, 6 (kernels_common.cuh "the other six schemes"): the code of each
+// weight is split into its top nibble (sign + 3 magnitude bits) and its low bits (none, a
+// per-weight LSB, two per-weight LSBs, or a group-shared LSB). The tile holds the nibbles in
+// 32-bit registers (8 per register: members i = 0..3 of a pair a | b) and the low bits in a
+// per-lane plane; see decode_frag for the exact bit positions the kernels expect.
+
+// bit position of member i's mag bit b (0..2) and sign, low half; E3 = the fp6-e3m2 map
+inline int nib_mag_pos(bool e3, int i, int b) {
+  if (!e3) return (9 - 3 * i) + b;
+  switch (i) {
+    case 0: return 10 + b;
+    case 1: return 4 + b;
+    case 2: return b;
+    default: return b == 0 ? 7 : b == 1 ? 8 : 3;
+  }
+}
+inline int nib_sign_pos(bool e3, int i) {
+  static constexpr int e2[4] = {15, 12, 13, 14}, e3p[4] = {15, 9, 13, 14};
+  return e3 ? e3p[i] : e2[i];
+}
+inline uint32_t nib_put(bool e3, int i, int half, unsigned nib) {
+  uint32_t r = 0;
+  for (int b = 0; b < 3; ++b) r |= ((nib >> b) & 1u) << (nib_mag_pos(e3, i, b) + 16 * half);
+  r |= ((nib >> 3) & 1u) << (nib_sign_pos(e3, i) + 16 * half);
+  return r;
+}
+inline unsigned nib_get(bool e3, int i, int half, uint32_t r) {
+  unsigned nib = 0;
+  for (int b = 0; b < 3; ++b) nib |= ((r >> (nib_mag_pos(e3, i, b) + 16 * half)) & 1u) << b;
+  nib |= ((r >> (nib_sign_pos(e3, i) + 16 * half)) & 1u) << 3;
+  return nib;
+}
+inline int low_bits_of(int id) { return id == 0 ? 0 : (id == 2 || id == 3) ? 2 : 1; }
+
+// The 16 x TK codes of tile (rt, kt) from the reference rows (0 past rows / padded_cols).
+void tile_codes(const DeviceLayout& L, const Scheme& s, const uint16_t* payload, size_t rt,
+                size_t kt, std::vector<uint8_t>& codes) {
+  const size_t TK = L.tk, blocks_per_tile = TK / static_cast<size_t>(s.block);
+  codes.assign(16 * TK, 0);
+  const size_t blk0 = kt * blocks_per_tile, nblk_row = L.padded_cols / static_cast<size_t>(s.block);
+  if (blk0 >= nblk_row) return;
+  const size_t nblk = std::min(blocks_per_tile, nblk_row - blk0);
+  for (size_t r = 0; r < 16; ++r) {
+    const size_t n = rt * 16 + r;
+    if (n >= L.rows) continue;
+    const uint16_t* w = payload + n * L.wpr + blk0 * static_cast<size_t>(s.words_per_block);
+    unpack_row(s, std::span<const uint16_t>(w, nblk * static_cast<size_t>(s.words_per_block)),
+               std::span<uint8_t>(codes.data() + r * TK, nblk * static_cast<size_t>(s.block)));
+  }
+}
+
+void tile_codes_store(const DeviceLayout& L, const Scheme& s, const std::vector<uint8_t>& codes,
+                      size_t rt, size_t kt, uint16_t* payload) {
+  const size_t TK = L.tk, blocks_per_tile = TK / static_cast<size_t>(s.block);
+  const size_t blk0 = kt * blocks_per_tile, nblk_row = L.padded_cols / static_cast<size_t>(s.block);
+  if (blk0 >= nblk_row) return;
+  const size_t nblk = std::min(blocks_per_tile, nblk_row - blk0);
+  for (size_t r = 0; r < 16; ++r) {
+    const size_t n = rt * 16 + r;
+    if (n >= L.rows) continue;
+    uint16_t* w = payload + n * L.wpr + blk0 * static_cast<size_t>(s.words_per_block);
+    pack_row(s, std::span<const uint8_t>(codes.data() + r * TK, nblk * static_cast<size_t>(s.block)),
+             std::span<uint16_t>(w, nblk * static_cast<size_t>(s.words_per_block)));
+  }
+}
+
+// (row, column) of output slot (q, i) of lane (g, t), half h (0 = a, 1 = b): family 4
+inline void fam4_rc(int g, int t, int q, int i, int h, int* row, int* col) {
+  *row = g + (q >= 2 ? 8 : 0);
+  *col = 16 * t + 8 * (q & 1) + 4 * h + i;
+}
+// family 7 (fp4.33): flat output f = 4q + i; pair k = f / 3, member m = f % 3
+inline void fam7_rc(int g, int t, int f, int h, int* row, int* col) {
+  const int k = f / 3, m = f - 3 * k;
+  *row = g + (k >= 2 ? 8 : 0);
+  *col = 12 * t + 6 * (k & 1) + 3 * h + m;
+}
+
+void nib_pack_tile(const DeviceLayout& L, const uint16_t* payload, size_t rt, size_t kt,
+                   uint8_t* tile) {
+  const int id = L.scheme_id;
+  const Scheme& s = scheme(id);
+  const bool e3 = id == 3;
+  const int lb = low_bits_of(id);
+  const size_t TK = L.tk;
+  std::vector<uint8_t> codes;
+  tile_codes(L, s, payload, rt, kt, codes);
+  std::memset(tile, 0, L.tile_bytes);
+  auto code = [&](int row, int col) -> unsigned { return codes[static_cast<size_t>(row) * TK + col]; };
+  for (int lane = 0; lane < 32; ++lane) {
+    const int g = lane >> 2, t = lane & 3;
+    if (id == 5) {
+      uint32_t R[3] = {0, 0, 0};
+      uint8_t sh = 0;
+      for (int f = 0; f < 12; ++f) {
+        for (int h = 0; h < 2; ++h) {
+          int row, col;
+          fam7_rc(g, t, f, h, &row, &col);
+          R[f >> 2] |= nib_put(false, f & 3, h, code(row, col) >> 1);
+          if (f % 3 == 0) sh = static_cast<uint8_t>(sh | (code(row, col) & 1u) << (f / 3 + 4 * h));
+        }
+      }
+      std::memcpy(tile + lane * 8, R, 8);
+      std::memcpy(tile + 256 + lane * 4, &R[2], 4);
+      tile[384 + lane] = sh;
+      continue;
+    }
+    uint32_t R[4] = {0, 0, 0, 0}, P = 0, Q[2] = {0, 0};
+    uint16_t sh16 = 0;
+    for (int q = 0; q < 4; ++q) {
+      for (int i = 0; i < 4; ++i) {
+        for (int h = 0; h < 2; ++h) {
+          int row, col;
+          fam4_rc(g, t, q, i, h, &row, &col);
+          const unsigned c = code(row, col);
+          R[q] |= nib_put(e3, i, h, c >> lb);
+          const int p = 4 * q + i;
+          if (id == 1) P |= (c & 1u) << (p + 16 * h);
+          if (id == 2 || id == 3) Q[p >> 3] |= (c & 3u) << (2 * (p & 7) + 16 * h);
+          if (id == 6 && (i == 0 || i == 2)) sh16 = static_cast<uint16_t>(sh16 | (c & 1u) << (8 * (i >> 1) + q + 4 * h));
+        }
+      }
+    }
+    std::memcpy(tile + lane * 16, R, 16);
+    if (id == 1) std::memcpy(tile + 512 + lane * 4, &P, 4);
+    if (id == 2 || id == 3) std::memcpy(tile + 512 + lane * 8, Q, 8);
+    if (id == 6) std::memcpy(tile + 512 + lane * 2, &sh16, 2);
+  }
+}
+
+void nib_unpack_tile(const DeviceLayout& L, const uint8_t* tile, size_t rt, size_t kt,
+                     uint16_t* payload) {
+  const int id = L.scheme_id;
+  const Scheme& s = scheme(id);
+  const bool e3 = id == 3;
+  const int lb = low_bits_of(id);
+  const size_t TK = L.tk;
+  std::vector<uint8_t> codes(16 * TK, 0);
+  auto set = [&](int row, int col, unsigned c) { codes[static_cast<size_t>(row) * TK + col] = static_cast<uint8_t>(c); };
+  for (int lane = 0; lane < 32; ++lane) {
+    const int g = lane >> 2, t = lane & 3;
+    if (id == 5) {
+      uint32_t R[3];
+      std::memcpy(R, tile + lane * 8, 8);
+      std::memcpy(&R[2], tile + 256 + lane * 4, 4);
+      const uint8_t sh = tile[384 + lane];
+      for (int f = 0; f < 12; ++f) {
+        for (int h = 0; h < 2; ++h) {
+          int row, col;
+          fam7_rc(g, t, f, h, &row, &col);
+          const unsigned shared = (sh >> (f / 3 + 4 * h)) & 1u;
+          set(row, col, nib_get(false, f & 3, h, R[f >> 2]) << 1 | shared);
+        }
+      }
+      continue;
+    }
+    uint32_t R[4], P = 0, Q[2] = {0, 0};
+    uint16_t sh16 = 0;
+    std::memcpy(R, tile + lane * 16, 16);
+    if (id == 1) std::memcpy(&P, tile + 512 + lane * 4, 4);
+    if (id == 2 || id == 3) std::memcpy(Q, tile + 512 + lane * 8, 8);
+    if (id == 6) std::memcpy(&sh16, tile + 512 + lane * 2, 2);
+    for (int q = 0; q < 4; ++q) {
+      for (int i = 0; i < 4; ++i) {
+        for (int h = 0; h < 2; ++h) {
+          int row, col;
+          fam4_rc(g, t, q, i, h, &row, &col);
+          unsigned c = nib_get(e3, i, h, R[q]) << lb;
+          const int p = 4 * q + i;
+          if (id == 1) c |= (P >> (p + 16 * h)) & 1u;
+          if (id == 2 || id == 3) c |= (Q[p >> 3] >> (2 * (p & 7) + 16 * h)) & 3u;
+          if (id == 6) c |= (sh16 >> (8 * (i >> 1) + q + 4 * h)) & 1u;
+          set(row, col, c);
+        }
+      }
+    }
+  }
+  tile_codes_store(L, s, codes, rt, kt, payload);
+}
+
 }  // namespace
 
 void repack_to_device(const DeviceLayout& L, const uint16_t* payload, uint8_t* out, int threads) {
@@ -236,8 +422,10 @@ void repack_to_device(const DeviceLayout& L, const uint16_t* payload, uint8_t* o
         uint8_t* tile = out + L.tile_offset(rt, kt);
         if (L.scheme_id == 4) {
           s4_pack_tile(L, payload, rt, kt, tile);
-        } else {
+        } else if (L.scheme_id == 7) {
           s7_pack_tile(L, payload, rt, kt, tile);
+        } else {
+          nib_pack_tile(L, payload, rt, kt, tile);
         }
       }
     }
@@ -251,8 +439,10 @@ void repack_from_device(const DeviceLayout& L, const uint8_t* in, uint16_t* payl
         const uint8_t* tile = in + L.tile_offset(rt, kt);
         if (L.scheme_id == 4) {
           s4_unpack_tile(L, tile, rt, kt, payload);
-        } else {
+        } else if (L.scheme_id == 7) {
           s7_unpack_tile(L, tile, rt, kt, payload);
+        } else {
+          nib_unpack_tile(L, tile, rt, kt, payload);
         }
       }
     }

@@ -1,0 +1,6 @@
+// k2_s1.cu -- K2 instances of scheme 1 (one translation unit per scheme: parallel builds).
+#include "k2.cuh"
+
+namespace amsqb {
+template cudaError_t launch_linear_scheme<1>(const LinearParams& p, cudaStream_t s);
+}  // namespace amsqb

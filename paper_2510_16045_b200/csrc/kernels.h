@@ -37,7 +37,14 @@ struct LinearParams {
   const unsigned short* scales;
   const unsigned short* x;  // [M][ldx] fp16 (logical cols)
   uint2* xperm;             // workspace: x in B-fragment order, [k_tiles][J][8*NB][4] units
-  unsigned short* y;        // [M][ldy] fp16
+  unsigned short* y;        // [M][ldy] fp16 (bf16 when yscale != null)
+  const float* yscale;      // bf16 activations: per batch row 2^-e (undoes amsq_x_bf16 scaling)
+  // fused tensor-parallel epilogue (amsq_linear_tp_fused; tp_ranks = 0: off): every output
+  // element also goes to column tp_col0 + n of each rank's [M][ldy] buffer tp_y[r] (peer
+  // memory over NVLink), and each CTA ends with a system-scope fence
+  int tp_ranks;
+  unsigned short* const* tp_y;  // device array [tp_ranks]
+  long long tp_col0;             // element offset of this launch's (m = 0, n = 0) in tp_y[r]
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
   int row_tiles, k_tiles;
@@ -51,7 +58,8 @@ struct TcParams {
   const uint8_t* w;
   const unsigned short* scales;
   const unsigned short* xk;  // workspace: activations prepped into [K/8][Np][8] (>= Np*KT*TK)
-  unsigned short* y;         // [M][ldy] fp16
+  unsigned short* y;         // [M][ldy] fp16 (bf16 when yscale != null)
+  const float* yscale;       // bf16 activations: per batch row 2^-e, or null
   long long rows, ldy;
   int M, Np;                 // batch rows; Np = round_up(M, 16) <= 256
   int row_tiles, k_tiles;
@@ -79,9 +87,24 @@ cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long lo
                              long long cols, cudaStream_t s);
 constexpr int kTcMaxBatch = 256;
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
+// Fused-TP flag barrier (one tiny launch per call): publish epoch e = *epoch + 1 into every
+// rank's flag array at index `rank`, wait until all ranks published e here, then *epoch = e.
+// Gives up after timeout_ns and sets *error (no hang on a missing peer).
+cudaError_t launch_tp_barrier(unsigned int* const* peer_flags, unsigned int* my_flags,
+                              unsigned int* epoch, unsigned int* error, int rank, int nranks,
+                              unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_unshard(const unsigned short* in, int P, int batch, int n, unsigned short* out,
                            cudaStream_t s);
+#ifndef AMSQ_K2_MAX_BATCH  // batch rows per K2 launch: 16 (NB <= 2) or 32 (NB = 4 for 17..32)
+#define AMSQ_K2_MAX_BATCH 32
+#endif
 int linear_max_batch_per_launch();
+// K2 for one scheme (k2.cuh; explicit instances in k2_s<id>.cu), batch <= AMSQ_K2_MAX_BATCH.
+template <int SCHEME>
+cudaError_t launch_linear_scheme(const LinearParams& p, cudaStream_t s);
+// bf16 activations -> fp16 scaled by 2^e per row (max |x| 2^e in [2^14, 2^15)); yscale[m] = 2^-e.
+cudaError_t launch_x_bf16_prep(const unsigned short* x, long long ldx, long long cols, int M,
+                               unsigned short* xh, float* yscale, cudaStream_t s);
 uint64_t kernel_launch_count();
 
 }  // namespace amsqb

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   auto store_y = [&](int m, float v) {
     if (m < p.M && n < p.rows) {
       const float sc = __half2float(__ushort_as_half(p.scales[n])) * kPlaceScale;
-      p.y[static_cast<long long>(m) * p.ldy + n] = __half_as_ushort(__float2half_rn(v * sc));
+      p.y[static_cast<long long>(m) * p.ldy + n] = out_bits(v * sc, p.yscale, m);
     }
   };
   if (warp < kTcEpiWarps && nst > 0) {

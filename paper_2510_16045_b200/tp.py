@@ -88,3 +88,68 @@ class ShardedLinear:
         return out
 
     __call__ = forward
+
+
+class FusedTPGroup:
+    """Single-process fused column-parallel group (amsq_tp_create_local): rank r's shard of a
+    weight runs amsq_linear_tp_fused, whose epilogue stores every output element into every
+    rank's arena over NVLink; a device-side flag barrier replaces the NCCL all-gather and the
+    unshard permutation. ``devices`` may repeat (virtual ranks on one GPU, for tests)."""
+
+    def __init__(self, devices, arena_bytes: int):
+        import ctypes as C
+        self.devices = list(devices)
+        self.nranks = len(self.devices)
+        self.arena_bytes = int(arena_bytes)
+        self._h = (C.c_void_p * self.nranks)()
+        devs = (C.c_int * self.nranks)(*self.devices)
+        check(lib().amsq_tp_create_local(self.nranks, devs, self.arena_bytes, self._h),
+              "tp_create_local")
+
+    def handle(self, rank: int) -> int:
+        return self._h[rank]
+
+    def arena(self, rank: int):
+        """This rank's arena as a uint8 torch tensor view (device memory owned by the group)."""
+        import ctypes as C
+        import torch
+        ptr, n = C.c_void_p(), C.c_size_t()
+        check(lib().amsq_tp_arena(self._h[rank], C.byref(ptr), C.byref(n)), "tp_arena")
+        return _device_view(ptr.value, n.value, self.devices[rank])
+
+    def linear(self, rank: int, shard: amsq.DeviceWeight, x, y_offset: int = 0, stream=None):
+        """Launch rank's fused linear on x ([M][K] fp16 on the rank's device)."""
+        import torch
+        st = stream.cuda_stream if stream is not None else \
+            torch.cuda.current_stream(self.devices[rank]).cuda_stream
+        check(lib().amsq_linear_tp_fused(shard.handle, self._h[rank], x.data_ptr(), x.shape[0],
+                                         y_offset, st), "linear_tp_fused")
+
+    def error(self, rank: int) -> int:
+        import ctypes as C
+        e = C.c_int(0)
+        check(lib().amsq_tp_error(self._h[rank], C.byref(e)), "tp_error")
+        return e.value
+
+    def close(self):
+        for r in range(self.nranks):
+            if self._h[r]:
+                lib().amsq_tp_destroy(self._h[r])
+                self._h[r] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(ptr: int, nbytes: int, device: int):
+    """A torch uint8 tensor aliasing device memory the library owns (no copy, no free)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=f"cuda:{device}")

@@ -13,7 +13,8 @@ from helpers import check_linear, gaussian_x, quantized_gaussian, random_payload
 
 pytestmark = pytest.mark.gpu
 
-SCHEMES = [4, 7]
+SCHEMES = list(range(8))  # every scheme of scheme.hpp:59-74 has sm_100a kernels
+AMS = [4, 7]              # the paper's two schemes (K3 tcgen05 path)
 SHAPES = [(1, 64), (33, 200), (40, 100), (16, 48), (300, 1000), (257, 4096), (512, 4098)]
 
 
@@ -211,7 +212,7 @@ def test_linear_k2_batch_chunks(cuda, orc, sid, shape, batch):
     check_linear(y, yref, yabs)
 
 
-@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("sid", AMS)
 @pytest.mark.parametrize("shape", [(128, 64), (300, 1000), (1000, 4098)])
 @pytest.mark.parametrize("batch", [24, 32, 64, 100, 256, 300])
 def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch, force_k3):
@@ -227,13 +228,27 @@ def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch, force_k3):
     check_linear(y, yref, yabs)
 
 
-@pytest.mark.parametrize("sid", SCHEMES)
+@pytest.mark.parametrize("sid", AMS)
 @pytest.mark.parametrize("batch", [17, 48, 112, 144, 200])
 def test_linear_tcgen05_cluster_split_odd_chunks(cuda, orc, sid, batch, force_k3):
     """K3 with a 2/4-CTA K split and a batch whose 16-column chunk count is odd."""
     rows, cols = 512, 2048 if sid == 4 else 2049
     qt = quantized_gaussian(sid, rows, cols, seed=batch)
     x = gaussian_x(batch, cols, seed=batch + 1)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
+@pytest.mark.parametrize("sid", [0, 1, 2, 3, 5, 6])
+@pytest.mark.parametrize("batch", [65, 100, 256])
+def test_other_schemes_large_batch_run_k2_chunks(cuda, orc, sid, batch):
+    """The six non-AMS schemes have no K3 instance: every batch runs K2 in 32-row chunks."""
+    rows, cols = 600, 2048
+    qt = random_payload(sid, rows, cols, seed=batch + sid)
+    x = gaussian_x(batch, cols, seed=batch)
     xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
     y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
     yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)

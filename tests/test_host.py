@@ -56,7 +56,7 @@ def test_schemes_match_reference_table(orc):
         name, blk, wpb, k, e, m, bias = SCHEMES[s.id]
         assert (s.name, s.block, s.words_per_block, s.k, s.exp_bits, s.man_bits, s.bias) == \
             (name, blk, wpb, k, e, m, bias)
-        assert s.device_supported == (s.id in (4, 7))
+        assert s.device_supported  # every scheme has sm_100a kernels
     assert amsq.scheme_by_name("fp5.33-e2m3").id == 7
     assert amsq.all_schemes()[4].effective_bits() == 4.25
     with pytest.raises(ValueError):
@@ -215,14 +215,14 @@ def _plan(sid, rows, cols):
     return tuple(plan)
 
 
-@pytest.mark.parametrize("sid", [4, 7])
+@pytest.mark.parametrize("sid", range(8))
 def test_work_plans_at_config_shapes(sid):
     """Every Llama-3.1-8B/70B (and TP-shard) shape gets a plan that covers its row tiles
     exactly, fits 148 SMs, keeps <= 64 row tiles per CTA and balances within 16 %."""
     shapes = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336), (10240, 8192),
               (8192, 8192), (57344, 8192), (8192, 28672), (1280, 8192), (1024, 8192),
               (7168, 8192), (1024, 28672), (33, 200), (1, 3)]
-    tk = 64 if sid == 4 else 48
+    tk = emulate.TRAITS[sid]["tk"]
     for rows, cols in shapes:
         n_groups, g_big, n_big, cs = _plan(sid, rows, cols)
         rt = -(-rows // 16)
@@ -239,7 +239,7 @@ LAYOUT_SHAPES = [(1, 3), (1, 64), (16, 48), (33, 200), (40, 100), (257, 4096), (
                  (17, 14336)]
 
 
-@pytest.mark.parametrize("sid", [4, 7])
+@pytest.mark.parametrize("sid", range(8))
 @pytest.mark.parametrize("shape", LAYOUT_SHAPES)
 def test_repack_is_exact_bit_permutation(sid, shape):
     rows, cols = shape
@@ -252,7 +252,7 @@ def test_repack_is_exact_bit_permutation(sid, shape):
     assert int(np.unpackbits(tiles).sum()) == int(np.unpackbits(qt.payload.view(np.uint8)).sum())
 
 
-@pytest.mark.parametrize("sid", [4, 7])
+@pytest.mark.parametrize("sid", range(8))
 @pytest.mark.parametrize("shape", [(16, 48), (33, 200), (300, 1000), (40, 4098)])
 def test_emulated_kernel_decode_restores_reference_grid(orc, sid, shape):
     """The tile bytes, decoded exactly as the sm_100a registers do (decode_s4/decode_s7 +
@@ -266,7 +266,7 @@ def test_emulated_kernel_decode_restores_reference_grid(orc, sid, shape):
     row_tiles = -(-rows // 16)
     k_tiles = -(-qt.padded_cols // tk)
     placed = emulate.placed_matrix(sid, tiles, row_tiles, k_tiles, _plan(sid, rows, cols))
-    grid = emulate.placed_to_grid(placed)[:rows, :qt.padded_cols]
+    grid = emulate.placed_to_grid(placed, sid)[:rows, :qt.padded_cols]
     want = orc.restore_grid(sid, rows, qt.padded_cols, qt.payload)
     # -0 codes place to 0x8000 and stay -0 after the exact rescale
     assert np.array_equal(grid, want)

@@ -189,3 +189,50 @@ def test_tp_nccl_rank_comm_and_linear_tp(cuda, orc):
     _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
     check_linear(y.cpu().numpy().view(np.uint16), yref, yabs)
     check(lib().amsq_nccl_comm_destroy(comm), "destroy")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sid", [4, 7])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_tp_fused_epilogue_matches_reference_and_nccl_path(cuda, orc, sid, P):
+    """§8(f)2: amsq_linear_tp_fused -- each rank's K2 epilogue stores its [M][N/P] slice into
+    EVERY rank's arena, then a flag barrier. With one GPU the P ranks are virtual (same
+    device, one stream each, launched concurrently); with P GPUs they are real peers. Every
+    rank must end with the identical full output, equal bit for bit to the per-shard K2
+    outputs concatenated (the NCCL path) and within the bar of the reference gemv. Two calls
+    at different arena offsets exercise the device-side epochs."""
+    from helpers import check_linear, gaussian_x, random_payload
+    from paper_2510_16045_b200 import DeviceWeight
+    ndev = torch.cuda.device_count()
+    devices = [r % ndev for r in range(P)]
+    n_local, cols = 512, 4096
+    rows = n_local * P
+    qt = random_payload(sid, rows, cols, seed=P + sid)
+    grp = tp.FusedTPGroup(devices, arena_bytes=2 * 2 * 40 * rows)
+    try:
+        shards = [DeviceWeight(qt, device=devices[r], row0=r * n_local, nrows=n_local)
+                  for r in range(P)]
+        streams = [torch.cuda.Stream(device=devices[r]) for r in range(P)]
+        for call, batch in enumerate((1, 40)):
+            x = gaussian_x(batch, cols, seed=batch)
+            xs = [torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(f"cuda:{d}")
+                  for d in devices]
+            off = call * 2 * 40 * rows
+            for r in range(P):
+                streams[r].wait_stream(torch.cuda.current_stream(devices[r]))
+                grp.linear(r, shards[r], xs[r], y_offset=off, stream=streams[r])
+            for s in streams:
+                s.synchronize()
+            assert all(grp.error(r) == 0 for r in range(P))
+            outs = [grp.arena(r)[off:off + 2 * batch * rows].view(torch.float16)
+                    .reshape(batch, rows).cpu() for r in range(P)]
+            for r in range(1, P):
+                assert torch.equal(outs[r], outs[0]), f"rank {r} differs"
+            local = torch.cat([shards[r].linear(xs[r]).cpu() for r in range(P)], dim=1)
+            assert torch.equal(outs[0], local)
+            yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+            _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x,
+                                   batch)
+            check_linear(outs[0].numpy().view(np.uint16), yref, yabs)
+    finally:
+        grp.close()
