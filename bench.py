@@ -531,6 +531,8 @@ def run_config4_tp(args, world, rank, local):
     ems = torch.tensor([a.elapsed_time(b)], device=dev)
     torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
     e2e_val = full_bytes * es / (float(ems.item()) * 1e-3) / 1e9
+    fused = _tp_fused_variant(args, sets, calls, xs, shapes, P, rank, local, stream, copies,
+                              full_bytes)
     peak, _, peak_kind = _peaks()
     per_rank_bytes = sum(shard_bytes[name] for name, m in calls)
     line = {
@@ -556,9 +558,61 @@ def run_config4_tp(args, world, rank, local):
                      "peak_src": peak_kind},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        "fused_tp": fused,
     }
     lib().amsq_nccl_comm_destroy(comm)
     return line
+
+
+def _tp_fused_variant(args, sets, calls, xs, shapes, P, rank, local, stream, copies, full_bytes):
+    """The same step through amsq_linear_tp_fused (K2 epilogue stores into every rank's arena
+    over NVLink + device flag barrier; CUDA-IPC segments exchanged with all_gather_object).
+    Reported beside the NCCL line; any failure is recorded, never fatal."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_16045_b200._lib import check, lib
+    try:
+        per_call = [2 * m * shapes[name][0] for name, m in calls]  # one arena region per call
+        offs = np.concatenate([[0], np.cumsum(per_call)]).astype(np.int64)
+        arena = int(offs[-1])
+        h = (C.c_uint8 * 64)()
+        tp = C.c_void_p()
+        check(lib().amsq_tp_segment_create(P, rank, local, arena, h, C.byref(tp)), "tp_segment")
+        allh = [None] * P
+        torch.distributed.all_gather_object(allh, bytes(h))
+        blob = (C.c_uint8 * (64 * P)).from_buffer_copy(b"".join(allh))
+        check(lib().amsq_tp_attach(tp, blob), "tp_attach")
+
+        def step(i):
+            ws = sets[i % copies]
+            for c, (name, m) in enumerate(calls):
+                rc = lib().amsq_linear_tp_fused(ws[name].handle, tp, xs[(name, m)].data_ptr(), m,
+                                                int(offs[c]), stream.cuda_stream)
+                if rc:
+                    raise RuntimeError(lib().amsq_last_error().decode())
+
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(args.steps):
+            step(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        err = C.c_int(0)
+        check(lib().amsq_tp_error(tp, C.byref(err)), "tp_error")
+        ms = torch.tensor([a.elapsed_time(b)], device=f"cuda:{local}")
+        torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+        lib().amsq_tp_destroy(tp)
+        t = float(ms.item())
+        return {"value": round(full_bytes * args.steps / (t * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "ms_per_step": round(t / args.steps, 4), "barrier_error": int(err.value)}
+    except Exception as e:  # noqa: BLE001 -- reported, the NCCL line stands
+        return {"error": f"{type(e).__name__}: {e}"[:200]}
 
 
 # ------------------------------------------------------------------ extras (--extra FILE)

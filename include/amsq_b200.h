@@ -169,6 +169,16 @@ int amsq_restore_to_host(amsq_weight_t h, int what, void* host_out, size_t bytes
  * workspace, so calls on one handle from different streams may overlap. */
 int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, void* stream);
 
+/* amsq_linear, and while it runs, the first stages of the NEXT call's weights (`next`, the
+ * weight of the call that follows on this stream; NULL = none) are pulled into L2, so that
+ * call's ramp starts from L2 instead of HBM (decode steps: layer after layer, graph-replayed).
+ * Results are identical to amsq_linear. */
+int amsq_linear_chain(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y,
+                      amsq_weight_t next, void* stream);
+/* Tuning knob: bytes per CTA amsq_linear_chain prefetches (default 64 KiB; 0 = off, < 0 only
+ * queries). Returns the previous value. Process-wide. */
+int amsq_debug_set_chain_prefetch(int bytes);
+
 /* Same with an explicit output row stride (elements) for writing into a wider buffer. */
 int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y,
                    size_t ldy, void* stream);

@@ -89,6 +89,8 @@ SIGNATURES = {
     "amsq_restore_f16": (_I, [_P, _P, _P]),
     "amsq_restore_to_host": (_I, [_P, _I, _P, _SZ, _P]),
     "amsq_linear": (_I, [_P, _P, _SZ, _P, _P]),
+    "amsq_linear_chain": (_I, [_P, _P, _SZ, _P, _P, _P]),
+    "amsq_debug_set_chain_prefetch": (_I, [_I]),
     "amsq_linear_ld": (_I, [_P, _P, _SZ, _P, _SZ, _P]),
     "amsq_linear_ex": (_I, [_P, _P, _I, _SZ, _P, _I, _SZ, _P]),
     "amsq_gemv_host": (_I, [_P, _U16P, _SZ, _SZ, _U16P, _P]),

@@ -58,6 +58,8 @@ unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA times
 // batches of at least this many rows run K3 (tcgen05); smaller ones run K2 in chunks of
 // linear_max_batch_per_launch() rows (measured crossover)
 std::atomic<int> g_k3_min_batch{65};
+// bytes of the successor's stream each CTA of amsq_linear_chain pulls into L2
+std::atomic<int> g_chain_pf_bytes{65536};
 
 struct CudaError : std::runtime_error {
   cudaError_t code;
@@ -238,7 +240,8 @@ struct TpArgs {
 };
 
 void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,
-                 cudaStream_t st, const float* yscale = nullptr, const TpArgs* tp = nullptr) {
+                 cudaStream_t st, const float* yscale = nullptr, const TpArgs* tp = nullptr,
+                 amsq_weight_t next = nullptr) {
   check_handle(h);
   if (batch == 0) throw amsqb::InvalidArgument("gemv: activation shape mismatch");
   if (!d_x || (!d_y && !tp)) throw amsqb::InvalidArgument("linear: null device buffer");
@@ -256,6 +259,13 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   p.k_tiles = static_cast<int>(h->L.k_tiles);
   p.plan = plan_of(h->L);
   p.trace = g_trace;
+  if (next && next->device == h->device && next->d_w) {
+    p.next_w = next->d_w;
+    p.next_plan = plan_of(next->L);
+    p.next_k_tiles = static_cast<int>(next->L.k_tiles);
+    p.next_tile_bytes = static_cast<int>(next->L.tile_bytes);
+    p.next_pf_bytes = g_chain_pf_bytes.load(std::memory_order_relaxed);
+  }
   if (tp) {
     p.tp_ranks = tp->nranks;
     p.tp_y = tp->d_y;
@@ -667,6 +677,20 @@ int amsq_linear(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_
     check_handle(h);
     linear_impl(h, d_x, batch, d_y, h->L.rows, as_stream(stream));
   });
+}
+
+int amsq_linear_chain(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y,
+                      amsq_weight_t next, void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    linear_impl(h, d_x, batch, d_y, h->L.rows, as_stream(stream), nullptr, nullptr, next);
+  });
+}
+
+int amsq_debug_set_chain_prefetch(int bytes) {
+  const int prev = g_chain_pf_bytes.load();
+  if (bytes >= 0) g_chain_pf_bytes.store(bytes);
+  return prev;
 }
 
 int amsq_linear_ld(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d_y, size_t ldy,

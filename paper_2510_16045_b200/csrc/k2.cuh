@@ -106,6 +106,12 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_CONSUMER_PROXY_FENCE  // consumers fence.proxy.async before releasing a stage
 #define AMSQ_CONSUMER_PROXY_FENCE 0
 #endif
+#ifndef AMSQ_K2_LEAN
+#define AMSQ_K2_LEAN 0
+#endif
+#ifndef AMSQ_EPI_OLD
+#define AMSQ_EPI_OLD 0
+#endif
 #ifndef AMSQ_TRACE_STAGES
 #define AMSQ_TRACE_STAGES 0
 #endif
@@ -405,6 +411,28 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
     stage_scales();
+    // the next call's first stages into L2 (its CTA j starts on an SM this grid frees): the
+    // same group / rank / rotation arithmetic as above, on the successor's plan
+    if (!AMSQ_K2_LEAN && p.next_w != nullptr && lane == 0) {
+      const GroupPlan& Q = p.next_plan;
+      const int nct = Q.n_groups * Q.csplit, KTn = p.next_k_tiles;
+      for (int b = blockIdx.x; b < nct; b += gridDim.x) {
+        const int gq = b / Q.csplit, rq = b - gq * Q.csplit;
+        const int Gq = Q.size(gq), kpq = (KTn + Q.csplit - 1) / Q.csplit;
+        const int kb2 = rq * kpq, ke2 = min(KTn, kb2 + kpq), L2n = ke2 - kb2;
+        if (L2n <= 0) continue;
+        const int rho2 = static_cast<int>(static_cast<long long>(gq) * L2n / Q.n_groups);
+        const long long tile_b = static_cast<long long>(Gq) * p.next_tile_bytes;  // one k-tile
+        const long long base = static_cast<long long>(Q.row0(gq)) * KTn * p.next_tile_bytes;
+        long long want = p.next_pf_bytes;
+        // from k-tile kb2 + rho2 to the end of the range, then wrapping to kb2
+        const long long run0 = min(want, (L2n - rho2) * tile_b) & ~15LL;
+        if (run0 > 0) bulk_prefetch_l2(p.next_w + base + (kb2 + rho2) * tile_b, static_cast<uint32_t>(run0));
+        want -= run0;
+        const long long run1 = min(want, rho2 * tile_b) & ~15LL;
+        if (run1 > 0) bulk_prefetch_l2(p.next_w + base + kb2 * tile_b, static_cast<uint32_t>(run1));
+      }
+    }
   } else {
     // ------------------------------------------------------------------ consumers
     // the warp's kpw k-tiles x NOWN row tiles of a stage, branch-free for a fixed NOWN
@@ -495,6 +523,71 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     // idle here, and wait for the peers' announcements before storing into theirs
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
+#if AMSQ_EPI_OLD  // A/B only: the round-1 epilogue (all 8*NB columns, integer indexing)
+  const int nslots = S / geo.kpw;               // k-slots (a warp covers kpw k-tiles of a stage)
+  float* red = reinterpret_cast<float*>(smem);  // [nslots][G][32][NB4]
+  constexpr int NB4 = NB * 4;
+  const int items = G * 32 * NB4;
+  if (warp < kConsumerWarps) {
+#pragma unroll
+    for (int i = 0; i < MAXOWN; ++i) {
+      if (i < nown) {
+        float* dst = red + (static_cast<long long>(ks) * G + rl + i * geo.wr) * 32 * NB4 + lane * NB4;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[nb * 4 + e] = acc[i][nb][e];
+      }
+    }
+  }
+  __syncthreads();
+  pdl_wait();  // outputs may still be read by the previous kernel
+  // clusters: recv[C][items] -- rank q's partial of the items rank r finalises lands in
+  // rank r's recv[q] (remote stores), one cluster barrier, then rank r sums in rank order
+  const int Gs = (G + CS - 1) / CS;  // row tiles each rank finalises
+  const int owned = Gs * 32 * NB4;   // items per rank
+  float* recv = reinterpret_cast<float*>(smem + geo.recv_off);  // [CS][owned]
+  auto store_y = [&](int it, float v) {
+    const int r = it / (32 * NB4), rem = it - r * 32 * NB4;
+    const int ln = rem / NB4, q = rem - ln * NB4, nb = q >> 2, e = q & 3;
+    const int m = nb * 8 + 2 * (ln & 3) + (e & 1);
+    const long long n = static_cast<long long>(rt0 + r) * 16 + (ln >> 2) + 8 * (e >> 1);
+    if (m < p.M && n < p.rows) {
+      const float sc = sscale[n - static_cast<long long>(rt0) * 16];
+      p.y[static_cast<long long>(m) * p.ldy + n] = out_bits(v * sc, p.yscale, m);
+    }
+  };
+  if (CS > 1 && geo.recv_in_ring) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    float v = 0.0f;
+    for (int k = 0; k < nslots; ++k) v += red[static_cast<long long>(k) * items + it];  // slot order
+    if constexpr (CS == 1) {
+      store_y(it, v);
+    } else {
+      const uint32_t owner = static_cast<uint32_t>((it / (32 * NB4)) / Gs);
+      float* dst = recv + static_cast<long long>(crank) * owned + (it - static_cast<int>(owner) * owned);
+      if (owner == crank) {
+        *dst = v;
+      } else {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(dst)), "r"(owner));
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+      }
+    }
+  }
+  if constexpr (CS > 1) {
+    __syncwarp();
+    cluster_sync_all();  // every rank's partials have landed in their owners' recv
+    const int i0 = min(G, static_cast<int>(crank) * Gs) * 32 * NB4;
+    const int i1 = min(G, static_cast<int>(crank + 1) * Gs) * 32 * NB4;
+    for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
+      float v = 0.0f;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) v += recv[static_cast<long long>(r) * owned + (it - i0)];  // rank order
+      store_y(it, v);
+    }
+  }
+#else
   // Only the M valid batch columns are reduced (at M = 1 that is 1/8 of the accumulator
   // elements), in a [slot][row tile][m][16 rows] layout, with no runtime integer division.
   const int nslots = S / geo.kpw;               // k-slots (a warp covers kpw k-tiles of a stage)
@@ -531,8 +624,14 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     const int m = q >> 4, row = q & 15;
     const long long n = static_cast<long long>(rt0 + r) * 16 + row;
     if (n < p.rows) {
+#if AMSQ_K2_LEAN  // A/B only: no bf16 / fused-TP epilogue branches
+      const unsigned short b = __half_as_ushort(__float2half_rn(v * sscale[r * 16 + row]));
+      constexpr bool tp_off = true;
+#else
       const unsigned short b = out_bits(v * sscale[r * 16 + row], p.yscale, m);
-      if (p.tp_ranks == 0) {
+      const bool tp_off = p.tp_ranks == 0;
+#endif
+      if (tp_off) {
         p.y[static_cast<long long>(m) * p.ldy + n] = b;
       } else {  // fused TP: the element lands in every rank's gathered output (NVLink stores)
         const long long off = static_cast<long long>(m) * p.ldy + p.tp_col0 + n;
@@ -586,6 +685,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       store_y(r, q, v);
     }
   }
+#endif
   if (p.tp_ranks) asm volatile("fence.acq_rel.sys;" ::: "memory");  // peer stores before the barrier
   if (trace && threadIdx.x == 0) trace[3] = globaltimer();
 }

@@ -45,6 +45,11 @@ struct LinearParams {
   int tp_ranks;
   unsigned short* const* tp_y;  // device array [tp_ranks]
   long long tp_col0;             // element offset of this launch's (m = 0, n = 0) in tp_y[r]
+  // cross-call L2 prefetch (amsq_linear_chain): once its last stage is issued, CTA j pulls the
+  // first next_pf_bytes of what CTA j (j + grid, ...) of the NEXT call will stream into L2
+  const uint8_t* next_w;        // null: off
+  GroupPlan next_plan;
+  int next_k_tiles, next_tile_bytes, next_pf_bytes;
   long long rows, cols, ldx, ldy;
   int M;                    // <= 16 per launch
   int row_tiles, k_tiles;
