@@ -84,6 +84,16 @@ int amsq_quantize_tensor(int scheme_id, size_t rows, size_t cols, const float* w
                          size_t* padded_cols, size_t* payload_words, uint16_t* scales,
                          uint16_t* payload);
 
+/* ---- device quantizer: quantize_tensor (quantize.hpp:188-216) on the GPU,
+ * bit-identical to amsq_quantize_tensor. d_w is device fp32 [rows][ldw] (ldw = 0: cols); the
+ * outputs are the reference stream in device memory: d_scales u16[rows], d_payload u16[words]
+ * (words = rows * words_per_row, see amsq_quantize_tensor's query). Synchronous: it waits for
+ * the stream to report a non-finite weight or a scale overflow as AMSQ_ECORRUPT (quantize.hpp:77,
+ * 89). */
+int amsq_quantize_device(int scheme_id, const float* d_w, size_t rows, size_t cols, size_t ldw,
+                         uint16_t* d_scales, uint16_t* d_payload, size_t words, int device,
+                         void* stream);
+
 /* ---- AMSQ container v1 (container.hpp:63-127), host buffers. */
 int amsq_container_size(int scheme_id, size_t rows, size_t cols, size_t* bytes);
 int amsq_container_write(int scheme_id, size_t rows, size_t cols, size_t padded_cols,

@@ -18,6 +18,7 @@ from .amsq import (  # noqa: F401
     pack_row,
     packed_payload_bytes,
     quantize_tensor,
+    quantize_tensor_device,
     read_amsq,
     restore_grid,
     restore_matrix,

@@ -192,6 +192,33 @@ def quantize_tensor(weights, scheme, threads: int = 1) -> QuantizedTensor:
     return QuantizedTensor(s, rows, cols, pc.value, scales, payload)
 
 
+def quantize_tensor_device(weights, scheme, device: int = 0, stream=None,
+                           to_host: bool = True):
+    """quantize_tensor on the GPU (amsq_quantize_device): bit-identical
+    scales and payload. `weights` is a CUDA float32 [rows][cols] tensor (or array-like, moved
+    to `device`). Returns a QuantizedTensor (host arrays) or, with to_host=False, the device
+    tensors (scales u16 as int16, payload u16 as int16) plus padded_cols."""
+    import torch
+    s = scheme_by_id(_sid(scheme))
+    w = torch.as_tensor(weights, dtype=torch.float32, device=f"cuda:{device}")
+    if w.ndim != 2 or w.numel() == 0:
+        raise ValueError("quantize_tensor: empty matrix")
+    w = w.contiguous()
+    rows, cols = w.shape
+    pc, nw = C.c_size_t(0), C.c_size_t(0)
+    check(lib().amsq_quantize_tensor(s.id, rows, cols, None, 1, C.byref(pc), C.byref(nw),
+                                     None, None), "quantize_tensor")
+    sc = torch.empty(rows, dtype=torch.int16, device=w.device)
+    pl = torch.empty(nw.value, dtype=torch.int16, device=w.device)
+    check(lib().amsq_quantize_device(s.id, w.data_ptr(), rows, cols, cols, sc.data_ptr(),
+                                     pl.data_ptr(), nw.value, device,
+                                     _stream_ptr(stream, device)), "quantize_device")
+    if not to_host:
+        return sc, pl, pc.value
+    return QuantizedTensor(s, rows, cols, pc.value, sc.cpu().numpy().view(np.uint16).copy(),
+                           pl.cpu().numpy().view(np.uint16).copy())
+
+
 # ------------------------------------------------------------------ container
 def write_amsq(qt: QuantizedTensor) -> bytes:
     """container.hpp:63-77 (returns the bytes instead of writing a stream)."""

@@ -439,6 +439,41 @@ int amsq_quantize_tensor(int id, size_t rows, size_t cols, const float* w, int t
   });
 }
 
+int amsq_quantize_device(int id, const float* d_w, size_t rows, size_t cols, size_t ldw,
+                         uint16_t* d_scales, uint16_t* d_payload, size_t words, int device,
+                         void* stream) {
+  return guarded([&] {
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    if (rows == 0 || cols == 0) throw amsqb::InvalidArgument("quantize_tensor: empty matrix");
+    if (ldw == 0) ldw = cols;
+    if (ldw < cols) throw amsqb::InvalidArgument("quantize_device: ldw < cols");
+    const size_t pc = amsqb::padded_cols(s, cols), wpr = amsqb::words_per_row(s, pc);
+    if (words != rows * wpr) throw amsqb::InvalidArgument("quantize_device: payload size mismatch");
+    if (!d_w || !d_scales || !d_payload) throw amsqb::InvalidArgument("quantize_device: null device buffer");
+    require_device(device);
+    DeviceGuard dg(device);
+    cudaStream_t st = as_stream(stream);
+    int* d_err = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d_err), sizeof(int), st), "cudaMallocAsync(err)");
+    ck(cudaMemsetAsync(d_err, 0, sizeof(int), st), "memset(err)");
+    static const amsqb::QuantTables kTables[amsqb::kNumSchemes] = {
+        amsqb::make_quant_tables(amsqb::scheme(0)), amsqb::make_quant_tables(amsqb::scheme(1)),
+        amsqb::make_quant_tables(amsqb::scheme(2)), amsqb::make_quant_tables(amsqb::scheme(3)),
+        amsqb::make_quant_tables(amsqb::scheme(4)), amsqb::make_quant_tables(amsqb::scheme(5)),
+        amsqb::make_quant_tables(amsqb::scheme(6)), amsqb::make_quant_tables(amsqb::scheme(7))};
+    ck(amsqb::launch_quantize(kTables[id], d_w, static_cast<long long>(rows), static_cast<long long>(ldw),
+                              static_cast<long long>(cols), static_cast<long long>(pc),
+                              static_cast<long long>(wpr), d_scales, d_payload, d_err, st),
+       "amsq_quantize_kernel launch");
+    int h_err = 0;
+    ck(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H err");
+    ck(cudaFreeAsync(d_err, st), "cudaFreeAsync(err)");
+    ck(cudaStreamSynchronize(st), "quantize sync");
+    if (h_err & 1) throw amsqb::Corrupt("non-finite weight");                       // quantize.hpp:77
+    if (h_err & 2) throw amsqb::Corrupt("channel scale overflows half precision");  // quantize.hpp:89
+  });
+}
+
 int amsq_container_size(int id, size_t rows, size_t cols, size_t* bytes) {
   return guarded([&] { *bytes = amsqb::container_bytes(amsqb::scheme(id), rows, cols); });
 }

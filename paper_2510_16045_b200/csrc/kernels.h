@@ -88,6 +88,23 @@ cudaError_t opt_in_max_smem(Kernel* fn, std::atomic<uint64_t>& done) {
 }
 
 cudaError_t launch_restore(const RestoreParams& p, cudaStream_t s);
+
+// Device quantize (quantize.cu): per-scheme value grid and packing map, passed by value.
+struct QuantTables {
+  int scheme_id, block, wpb, segs, k, sign_mask, ngrid, nshared;
+  float maxmag;
+  float val[64];      // value of each raw code (format.hpp:82-93)
+  float grid_v[64];   // sorted grid (format.hpp:119-131) and its codes
+  uint8_t grid_c[64];
+  uint8_t seg_word[128], seg_bit[128], seg_width[128], seg_shift[128];  // [weight * segs + j]
+  uint8_t sh_word[16], sh_bit[16];                                      // shared slot of group g
+};
+struct Scheme;
+QuantTables make_quant_tables(const Scheme& s);
+// err: device int, OR-ed with 1 (non-finite weight) / 2 (scale overflows binary16).
+cudaError_t launch_quantize(const QuantTables& tb, const float* w, long long rows, long long ldw,
+                            long long cols, long long pc, long long wpr, unsigned short* scales,
+                            unsigned short* payload, int* err, cudaStream_t s);
 cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
                              long long cols, cudaStream_t s);
 constexpr int kTcMaxBatch = 256;

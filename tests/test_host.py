@@ -286,6 +286,10 @@ def test_device_entry_points_fail_loudly_without_gpu():
     h = C.c_void_p(None)
     rc = lib().amsq_linear(h, None, 1, None, None)
     assert rc != 0
+    # the device quantizer: valid arguments, no device -> AMSQ_ENODEV (never the host path)
+    fake = C.c_void_p(256)
+    from paper_2510_16045_b200._lib import AMSQ_ENODEV
+    assert lib().amsq_quantize_device(7, fake, 4, 6, 6, fake, fake, 8, 0, None) == AMSQ_ENODEV
 
 
 def test_container_file_upload_validates_before_the_device(tmp_path):
