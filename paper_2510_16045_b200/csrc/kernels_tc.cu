@@ -22,6 +22,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -34,11 +35,25 @@ void count_launch();
 
 namespace dev {
 
-// Natural column (within a k-tile) of the p-th fp16 a decode lane run emits. A lane (g, t)
-// covers columns [12t, 12t + 12) (FP5.33) / [16t, 16t + 16) (FP4.25) of its rows and emits
-// them as the pairs of decode_s7 / decode_s4 (kernels_common.cuh).
+#ifndef AMSQ_TC_ATMEM  // 1: the decoded A operand lives in TMEM (tcgen05.st); 0: shared memory
+#define AMSQ_TC_ATMEM 1
+#endif
+
+// Natural column (within a k-tile) of logical K position p of the decoded A operand.
+//  * A in TMEM: decode warp lane (g, t) stores MMA j's fragment {A0, A2, A1, A3} with
+//    tcgen05.st.16x256b (measured map, tools/tmem_probe.cu: register r -> TMEM lane g + 8 (r >> 1),
+//    column 2t + (r & 1)), and the MMA reads column c as K = 2c, 2c + 1. So K position
+//    L = p mod 16 of MMA j = p / 16 is lane t = L / 4's mma.sync slot s = 2 ((L / 2) & 1) + (L & 1),
+//    i.e. natural column t * kLaneK + kofs(j, s) -- the B-fragment columns of K2 (bfrag_s4/_s7).
+//  * A in shared memory: a lane (g, t) covers columns [12t, 12t + 12) (FP5.33) / [16t, 16t + 16)
+//    (FP4.25) of its rows and emits them as the pairs of decode_s7 / decode_s4.
 template <int SCHEME>
-__host__ __device__ __forceinline__ int tc_kperm(int p) {
+__device__ __forceinline__ int tc_kperm(int p) {
+#if AMSQ_TC_ATMEM
+  using T = Traits<SCHEME>;
+  const int j = p >> 4, L = p & 15;
+  return (L >> 2) * T::kLaneK + T::kofs(j, ((L >> 1) & 1) * 2 + (L & 1));
+#else
   if constexpr (SCHEME == 7) {
     const int t = p / 12, r = p - 12 * t;
     const int q = r / 6, i = (r - 6 * q) >> 1, h = r & 1;
@@ -48,6 +63,7 @@ __host__ __device__ __forceinline__ int tc_kperm(int p) {
     const int q = r >> 3, j = (r & 7) >> 1, h = r & 1;
     return 16 * t + 8 * q + 4 * h + j;
   }
+#endif
 }
 
 // x[M][ldx] -> xk[KTOT/8][Np][8] (the UMMA no-swizzle K-major image), K permuted per tile.
@@ -90,6 +106,24 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a, uint64_t
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] . B[smem desc]: the A operand read from tensor memory (128 lanes = rows,
+// consecutive 32-bit columns = K pairs)
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// one m16 x k16 A fragment into TMEM lanes [lane0, lane0 + 16) x 8 columns (mma.sync fragment order)
+__device__ __forceinline__ void tc_st_frag(uint32_t taddr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a0), "r"(a1),
+               "r"(a2), "r"(a3)
+               : "memory");
+}
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -124,8 +158,10 @@ struct TcGeom {
   int stages;
   int a_bytes;  // A buffer per stage: 128 rows x kchunk*TK fp16
   int b_bytes;  // B buffer per stage: Np rows x kchunk*TK fp16
-  int stage;    // A + activation image + weight tiles (8 row tiles x kchunk), 1 KB aligned
+  int stage;    // [A +] activation image + weight tiles (8 row tiles x kchunk), 1 KB aligned
   int tmem_cols;
+  int a_col0;   // A in TMEM: first column of stage 0's A (after the Np accumulator columns)
+  int cols_a;   // A in TMEM: columns per stage (kchunk * TK / 2 fp16 pairs)
 };
 
 __device__ __forceinline__ uint32_t tc_cluster_rank() {
@@ -216,8 +252,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 
   if (warp < kTcDecodeWarps) {
     // ------------------------------------------------------------------ decode warps
-    // warp w: row tile rb0 + (w & 7), the k-tiles of parity w >> 3 of every stage
+    // warp w: the k-tiles of parity w >> 3 of every stage, for row tile rtl. With A in TMEM a warp
+    // may only touch TMEM lanes 32 (w % 4) .. + 31, i.e. row tiles 2 (w % 4) and 2 (w % 4) + 1.
+#if AMSQ_TC_ATMEM
+    const int rtl = 2 * (warp & 3) + ((warp >> 2) & 1), par = warp >> 3;
+#else
     const int rtl = warp & 7, par = warp >> 3;
+#endif
     const bool live = rb0 + rtl < rb1;
     const int g = lane >> 2, t = lane & 3;
     // where this row tile sits in a stage's weight buffer: segment base + [kk][row in segment]
@@ -246,6 +287,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       const uint8_t* W = A + geo.a_bytes + geo.b_bytes + wbase;
       for (int kk = par; kk < geo.kchunk; kk += 2) {
         if (kb + st * geo.kchunk + kk < ke) {
+#if AMSQ_TC_ATMEM
+          if (!live) continue;  // rows past the tensor: D rows that are never stored
+          const uint8_t* tp = W + (kk * srows + sr) * TILE;
+          const uint4 wv = *reinterpret_cast<const uint4*>(tp + lane * 16);
+          const uint32_t sh = SCHEME == 4 ? tp[512 + lane] : 0u;
+          uint32_t Af[J][4];
+          const uint32_t R[4] = {wv.x, wv.y, wv.z, wv.w};
+          if constexpr (SCHEME == 4) {
+            decode_s4(R, sh, Af);
+          } else {
+            decode_s7(R, Af);
+          }
+          const uint32_t ta = tmem + (static_cast<uint32_t>(rtl * 16) << 16) +
+                              static_cast<uint32_t>(geo.a_col0 + sidx * geo.cols_a + kk * J * 8);
+#pragma unroll
+          for (int j = 0; j < J; ++j) tc_st_frag(ta + j * 8, Af[j][0], Af[j][2], Af[j][1], Af[j][3]);
+#else
           uint4 wv = make_uint4(0, 0, 0, 0);
           uint32_t sh = 0;
           if (live) {
@@ -290,9 +348,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
               *reinterpret_cast<uint4*>(A + ((c0 >> 3) + 1) * lboA + r * 16) = make_uint4(v[2], v[3], v[4], v[5]);
             }
           }
+#endif
         }
       }
-#ifndef AMSQ_TC_NOFENCE  // profiling variant only: drops the generic->async proxy fence
+#if AMSQ_TC_ATMEM
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();  // the TMEM stores, before the arrival the MMA thread acquires
+#else
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
 #endif
       __syncwarp();
@@ -362,9 +424,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
         const uint32_t a0 = smem_u32(smem + sidx * geo.stage);
         const uint32_t b0 = a0 + geo.a_bytes;
         for (int k16 = 0; k16 < nk * TK / 16; ++k16) {
-          const uint64_t ad = umma_desc(a0 + k16 * 2 * lboA, lboA, 128);
           const uint64_t bd = umma_desc(b0 + k16 * 2 * lboB, lboB, 128);
+#if AMSQ_TC_ATMEM
+          const uint32_t at = tmem + static_cast<uint32_t>(geo.a_col0 + sidx * geo.cols_a + k16 * 8);
+          tc_mma_f16_ts(tmem, at, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+#else
+          const uint64_t ad = umma_desc(a0 + k16 * 2 * lboA, lboA, 128);
           tc_mma_f16(tmem, ad, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+#endif
         }
         tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
         if (tr8 && st < 8) trace[48 + st] = clock64();
@@ -522,18 +589,24 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   const int budget = 227 * 1024 - 2048;
   for (int kc : {4, 2}) {  // k-tiles per stage (even: two decode warps per row tile)
     geo.kchunk = kc;
-    geo.a_bytes = 128 * kc * T::kTK * 2;
+    geo.a_bytes = AMSQ_TC_ATMEM ? 0 : 128 * kc * T::kTK * 2;
     geo.b_bytes = p.Np * kc * T::kTK * 2;
     geo.stage = (geo.a_bytes + geo.b_bytes + 8 * kc * T::kTileBytes + 1023) / 1024 * 1024;
     geo.stages = budget / geo.stage;
+    if (AMSQ_TC_ATMEM) {  // the A ring shares TMEM with the Np accumulator columns
+      geo.a_col0 = p.Np <= 128 ? 128 : 256;
+      geo.cols_a = kc * T::kTK / 2;
+      geo.stages = std::min(geo.stages, (512 - geo.a_col0) / geo.cols_a);
+    }
     if (geo.stages >= 4 || geo.stages > best.stages) best = geo;
     if (geo.stages >= 4) break;
   }
   geo = best;
-  if (geo.stages > 6) geo.stages = 6;
+  if (geo.stages > (AMSQ_TC_ATMEM ? 8 : 6)) geo.stages = AMSQ_TC_ATMEM ? 8 : 6;
   if (geo.stages < 2) return cudaErrorInvalidConfiguration;
   geo.tmem_cols = 32;
   while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
+  if (AMSQ_TC_ATMEM) geo.tmem_cols = 512;
   const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16 + dev::kTcMaxSeg * 16;
   // split K over a cluster when the 128-row blocks alone leave SMs idle
   const int rb = (p.row_tiles + 7) / 8;
