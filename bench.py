@@ -641,7 +641,6 @@ def run_batch_sweep(args, dev, stream, cap):
                                        stream, cap)
         del dense
     torch.cuda.empty_cache()
-    k3_min = lib().amsq_debug_set_k3_min_batch(0)
     for scheme in ("fp5.33-e2m3", "fp4.25-e2m2"):
         for i, (name, (n, k)) in enumerate(shapes.items()):
             ws = _rotation(amsq.DeviceWeight(_qt(scheme, n, k, seed=500 + i), device=dev.index))
@@ -654,7 +653,7 @@ def run_batch_sweep(args, dev, stream, cap):
                                2 * len(ws), 5, stream, cap)
                 flops = 2.0 * m * n * k
                 out.append({"scheme": scheme, "layer": name, "M": m,
-                            "kernel": "K3" if m >= k3_min else "K2",
+                            "kernel": "K3" if lib().amsq_linear_uses_tc(ws[0].scheme.id, m) else "K2",
                             "us": round(us, 2), "packed_GBps": round(pb / us / 1e3, 1),
                             "hbm_frac": round(algorithmic_bytes(pb, n, k, m) / us / 1e3 / peak, 3),
                             "TFLOPs": round(flops / us / 1e6, 1),

@@ -265,10 +265,13 @@ uint64_t amsq_kernel_launch_count(void);
  * each fused-linear CTA (0 start, 1 first stage landed, 2 stream done, 3 end, 4..7 the
  * producer's first issues, 8+2s / 9+2s stage s landed / consumed); NULL = off. */
 void amsq_debug_set_trace(void* d_buf);
-/* Dispatch knob: batches of >= rows run the tcgen05 kernel (K3), smaller ones the mma.sync
- * kernel (K2) in 32-row chunks. rows <= 0 only queries; values below 17 clamp to 17. Returns
- * the previous threshold (default 65, the measured crossover). Process-wide. */
+/* Dispatch knob: batches of >= rows run the tcgen05 kernel (K3, schemes 4 and 7), smaller ones
+ * the mma.sync kernel (K2) in 32-row chunks. rows > 0 overrides the per-scheme measured crossover
+ * (FP5.33: 48, FP4.25: 65), rows < 0 restores it, 0 only queries. Returns the previous setting
+ * (-1 = the per-scheme defaults). Process-wide. */
 int amsq_debug_set_k3_min_batch(int rows);
+/* 1 when amsq_linear on a batch of `batch` rows of this scheme runs K3 (tcgen05), 0 for K2. */
+int amsq_linear_uses_tc(int scheme_id, size_t batch);
 
 #ifdef __cplusplus
 }

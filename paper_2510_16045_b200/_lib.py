@@ -112,6 +112,7 @@ SIGNATURES = {
     "amsq_kernel_launch_count": (C.c_uint64, []),
     "amsq_debug_set_trace": (None, [_P]),
     "amsq_debug_set_k3_min_batch": (_I, [_I]),
+    "amsq_linear_uses_tc": (_I, [_I, _SZ]),
 }
 
 _lib = None

@@ -57,7 +57,19 @@ thread_local std::string g_error;
 unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
 // batches of at least this many rows run K3 (tcgen05); smaller ones run K2 in chunks of
 // linear_max_batch_per_launch() rows (measured crossover)
-std::atomic<int> g_k3_min_batch{65};
+std::atomic<int> g_k3_min_batch{-1};  // > 0: a process-wide override of k3_min_batch()
+
+// Batches of at least this many rows run K3 (tcgen05), smaller ones K2 in 32-row chunks: the
+// measured crossover per scheme (profiles/r02/k3_small_m.txt: with the A operand in TMEM, K3 wins
+// FP5.33 from M = 48 on; FP4.25's gate_up still prefers two K2 launches at M = 64).
+int k3_min_batch(int scheme_id) {
+  const int v = g_k3_min_batch.load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  return scheme_id == 7 ? 48 : 65;
+}
+bool uses_k3(int scheme_id, size_t batch) {
+  return (scheme_id == 4 || scheme_id == 7) && batch >= static_cast<size_t>(k3_min_batch(scheme_id));
+}
 // bytes of the successor's stream each CTA of amsq_linear_chain pulls into L2
 std::atomic<int> g_chain_pf_bytes{65536};
 
@@ -271,8 +283,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
     p.tp_y = tp->d_y;
     p.tp_col0 = tp->col0;
   }
-  const bool k3_scheme = h->L.scheme_id == 4 || h->L.scheme_id == 7;  // K3: the two AMS schemes
-  if (!tp && k3_scheme && batch >= static_cast<size_t>(g_k3_min_batch.load(std::memory_order_relaxed))) {
+  if (!tp && uses_k3(h->L.scheme_id, batch)) {  // K3: the two AMS schemes
     // K3: tcgen05 tiles, up to 256 batch rows per launch (weights streamed once per launch)
     // the activation image is stream-ordered scratch (cudaMallocAsync: capturable in CUDA
     // graphs, pooled, and private to this call -- no race between streams)
@@ -1073,8 +1084,10 @@ void amsq_debug_set_trace(void* d_buf) { g_trace = static_cast<unsigned long lon
 
 int amsq_debug_set_k3_min_batch(int rows) {
   const int prev = g_k3_min_batch.load();
-  if (rows > 0) g_k3_min_batch.store(rows < 17 ? 17 : rows);
+  if (rows != 0) g_k3_min_batch.store(rows > 0 ? rows : -1);
   return prev;
 }
+
+int amsq_linear_uses_tc(int scheme_id, size_t batch) { return uses_k3(scheme_id, batch) ? 1 : 0; }
 
 }  // extern "C"

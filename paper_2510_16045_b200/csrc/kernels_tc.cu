@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 #if AMSQ_TC_ATMEM
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();  // the TMEM stores, before the arrival the MMA thread acquires
+      // the generic-proxy reads of this stage's weight tiles, before the producer's bulk copy
+      // (async proxy) rewrites the stage once the MMAs release it (cross-proxy WAR)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #else
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor core
 #endif

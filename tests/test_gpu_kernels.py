@@ -189,9 +189,25 @@ def test_cpp_dropin_against_reference(cuda):
 
 @pytest.fixture
 def force_k3():
-    """Route every batch > 16 to K3 (default: K2 in 32-row chunks below 65 rows)."""
+    """Route every batch > 16 to K3 (default: K2 in 32-row chunks below the per-scheme crossover)."""
     from paper_2510_16045_b200._lib import lib
     prev = lib().amsq_debug_set_k3_min_batch(17)
+    yield
+    lib().amsq_debug_set_k3_min_batch(prev)
+
+
+@pytest.fixture
+def force_k3_all():
+    from paper_2510_16045_b200._lib import lib
+    prev = lib().amsq_debug_set_k3_min_batch(1)
+    yield
+    lib().amsq_debug_set_k3_min_batch(prev)
+
+
+@pytest.fixture
+def force_k2():
+    from paper_2510_16045_b200._lib import lib
+    prev = lib().amsq_debug_set_k3_min_batch(100000)
     yield
     lib().amsq_debug_set_k3_min_batch(prev)
 
@@ -199,7 +215,7 @@ def force_k3():
 @pytest.mark.parametrize("sid", SCHEMES)
 @pytest.mark.parametrize("shape", [(33, 200), (300, 1000), (1000, 4098), (80000, 64)])
 @pytest.mark.parametrize("batch", [17, 24, 31, 32, 40, 64])
-def test_linear_k2_batch_chunks(cuda, orc, sid, shape, batch):
+def test_linear_k2_batch_chunks(cuda, orc, sid, shape, batch, force_k2):
     """17 <= M < 65 runs K2 in 32-row chunks (M <= 32: the NB = 4 kernel; groups taller than
     32 row tiles fall back to two M <= 16 launches)."""
     rows, cols = shape
@@ -223,6 +239,22 @@ def test_linear_large_batch_tcgen05(cuda, orc, sid, shape, batch, force_k3):
     dw = amsq.DeviceWeight(qt)
     xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
     y = dw.linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
+@pytest.mark.parametrize("sid", AMS)
+@pytest.mark.parametrize("shape", [(128, 64), (300, 1000), (4096, 4098)])
+@pytest.mark.parametrize("batch", [1, 5, 16])
+def test_linear_tcgen05_small_batch(cuda, orc, sid, shape, batch, force_k3_all):
+    """K3 below 16 rows (one 16-column N chunk, zero-padded batch rows): the A-in-TMEM MMA path
+    at the smallest N the kind::f16 instruction takes."""
+    rows, cols = shape
+    qt = quantized_gaussian(sid, rows, cols, seed=batch * 7 + rows)
+    x = gaussian_x(batch, cols, seed=batch + 3)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
     yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
     _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
     check_linear(y, yref, yabs)

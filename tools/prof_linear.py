@@ -28,7 +28,11 @@ def main():
     ap.add_argument("--cublas", action="store_true")
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--empty", action="store_true", help="time an empty kernel per call")
+    ap.add_argument("--k3min", type=int, default=0, help="K3 dispatch threshold (0: default)")
     args = ap.parse_args()
+    if args.k3min > 0:
+        from paper_2510_16045_b200._lib import lib
+        lib().amsq_debug_set_k3_min_batch(args.k3min)
     sid = amsq.scheme_by_name(args.scheme).id
     copies = max(2, int(np.ceil(260e6 / amsq.packed_payload_bytes(sid, args.n, args.k))))
     ws = [amsq.DeviceWeight(bench._qt(args.scheme, args.n, args.k, seed=c)) for c in range(copies)]

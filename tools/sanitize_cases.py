@@ -26,6 +26,8 @@ CASES = [  # (scheme, rows, cols, batch, k3)
     (7, 2560, 8192, 12, False),    # C=4, xprep (M <= 16)
     (7, 1024, 2049, 32, False),    # NB=4 (M <= 32)
     (4, 512, 2048, 48, True),      # K3 tcgen05, 2-CTA split-K
+    (7, 1024, 4096, 5, True),      # K3 with one 16-column N chunk (A in TMEM, M < 16)
+    (7, 2048, 2048, 128, True),    # K3 C=1, 8 N chunks
 ]
 
 
@@ -34,7 +36,7 @@ def main():
     orc = COracle()
     for i in only:
         sid, rows, cols, batch, k3 = CASES[i]
-        prev = lib().amsq_debug_set_k3_min_batch(17 if k3 else 65)
+        prev = lib().amsq_debug_set_k3_min_batch(1 if k3 else 100000)
         qt = random_payload(sid, rows, cols, seed=i)
         dw = amsq.DeviceWeight(qt)
         x = gaussian_x(batch, cols, seed=i)
