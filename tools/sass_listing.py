@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Dump the SASS of the product kernels (cuobjdump -sass) into profiles/<round>/sass/ with an
 opcode histogram per kernel: the evidence that K2 issues HMMA + TMA bulk (UBLKCP) and K3
-issues tcgen05 (UTCHMMA / LDTM / UTCBAR / UTCATOMSWS) and cluster DSMEM traffic."""
+issues tcgen05 (UTCHMMA / STTM = tcgen05.st of the decoded A operand / LDTM / UTCBAR / UTCATOMSWS)
+and cluster DSMEM traffic."""
 import collections
 import os
 import re
@@ -14,8 +15,9 @@ OUT = os.path.join(ROOT, "profiles", sys.argv[1] if len(sys.argv) > 1 else "r01"
 KEEP = ["amsq_linear_kernelILi7ELi1ELi1E", "amsq_linear_kernelILi7ELi1ELi2E",
         "amsq_linear_kernelILi4ELi1ELi2E", "amsq_linear_kernelILi7ELi2ELi2E",
         "amsq_linear_kernelILi7ELi4ELi1E",
-        "amsq_linear_tc_kernelILi7ELi4E", "amsq_linear_tc_kernelILi4ELi1E",
-        "amsq_restore_kernelILi7E", "amsq_xprep_tc_kernelILi7E"]
+        "amsq_linear_tc_kernelILi7ELi4E", "amsq_linear_tc_kernelILi7ELi1E",
+        "amsq_linear_tc_kernelILi4ELi1E", "amsq_restore_kernelILi7E", "amsq_xprep_tc_kernelILi7E",
+        "amsq_quantize_kernel"]
 
 
 def main():
@@ -39,7 +41,7 @@ def main():
         with open(os.path.join(OUT, short + ".sass"), "w") as fh:
             fh.write("Function : " + "\n".join(lines) + "\n")
         key = {k: ops.get(k, 0) for k in ("HMMA", "UTCHMMA", "UBLKCP", "LDTM", "UTCBAR",
-                                          "UTCATOMSWS", "LDGSTS", "SYNCS", "LOP3", "IMAD", "PRMT")}
+                                          "UTCATOMSWS", "STTM", "LDGSTS", "SYNCS", "LOP3", "IMAD", "PRMT")}
         summary.append(f"{short}: {sum(ops.values())} instructions; " +
                        ", ".join(f"{k} {v}" for k, v in key.items() if v))
     with open(os.path.join(OUT, "SUMMARY.txt"), "w") as fh:
