@@ -94,6 +94,13 @@ int amsq_quantize_device(int scheme_id, const float* d_w, size_t rows, size_t co
                          uint16_t* d_scales, uint16_t* d_payload, size_t words, int device,
                          void* stream);
 
+/* The same with host buffers (the reference's quantize_tensor call shape): w is host fp32
+ * [rows][cols]; pass scales == payload == NULL to query *padded_cols and *payload_words.
+ * Synchronous (its own stream). */
+int amsq_quantize_device_host(int scheme_id, size_t rows, size_t cols, const float* w, int device,
+                              size_t* padded_cols, size_t* payload_words, uint16_t* scales,
+                              uint16_t* payload);
+
 /* ---- AMSQ container v1 (container.hpp:63-127), host buffers. */
 int amsq_container_size(int scheme_id, size_t rows, size_t cols, size_t* bytes);
 int amsq_container_write(int scheme_id, size_t rows, size_t cols, size_t padded_cols,

@@ -9,6 +9,8 @@
  *   amsq::restore_matrix(qt, threads)            -> amsq_b200::restore_matrix<Matrix>(qt)
  *   amsq::restore_matrix_half(qt, threads)       -> amsq_b200::restore_matrix_half(qt)
  *   amsq::restore_block(words, layout, table, o) -> DeviceTensor::restore_grid()
+ *   amsq::quantize_tensor(w, scheme, threads)    -> amsq_b200::quantize_tensor<QT>(w, scheme)
+ *                                                   (on the GPU, bit-identical)
  *   (resident weights, the serving path)         -> amsq_b200::DeviceTensor
  *
  * `QT` is any type with the fields of amsq::QuantizedTensor (quantize.hpp:45-61):
@@ -153,6 +155,30 @@ std::vector<uint16_t> restore_matrix_half(const QT& qt, int /*threads*/ = 1) {
   std::vector<uint16_t> out(b.size() / 2);
   std::memcpy(out.data(), b.data(), b.size());
   return out;
+}
+
+// quantize.hpp:188-216 quantize_tensor(weights, scheme, threads), on the GPU
+// (amsq_quantize_device_host): bit-identical scales and payload. MatrixT has the reference
+// Matrix's `rows`, `cols` and contiguous fp32 `data`; QT is default-constructible with the
+// QuantizedTensor fields, and `scheme` must outlive it (as scheme_by_id's static schemes do).
+template <class QT, class MatrixT, class SchemeT>
+QT quantize_tensor(const MatrixT& weights, const SchemeT& scheme, int /*threads*/ = 1, int device = 0) {
+  const int id = static_cast<int>(scheme.id);
+  size_t pc = 0, words = 0;
+  check(amsq_quantize_device_host(id, weights.rows, weights.cols, nullptr, device, &pc, &words, nullptr,
+                                  nullptr),
+        "quantize_tensor");
+  QT qt;
+  qt.scheme = &scheme;
+  qt.rows = weights.rows;
+  qt.cols = weights.cols;
+  qt.padded_cols = pc;
+  qt.scales.assign(weights.rows, 0);
+  qt.payload.assign(words, 0);
+  check(amsq_quantize_device_host(id, weights.rows, weights.cols, weights.data.data(), device, &pc, &words,
+                                  qt.scales.data(), qt.payload.data()),
+        "quantize_tensor");
+  return qt;
 }
 
 // restore_block over the whole tensor (kernels.hpp:55-63): grid bits, [rows][padded_cols].

@@ -68,6 +68,7 @@ SIGNATURES = {
     "amsq_quantize_tensor": (_I, [_I, _SZ, _SZ, _P, _I, C.POINTER(_SZ), C.POINTER(_SZ), _U16P,
                                   _U16P]),
     "amsq_quantize_device": (_I, [_I, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _I, _P]),
+    "amsq_quantize_device_host": (_I, [_I, _SZ, _SZ, _P, _I, C.POINTER(_SZ), C.POINTER(_SZ), _P, _P]),
     "amsq_container_size": (_I, [_I, _SZ, _SZ, C.POINTER(_SZ)]),
     "amsq_container_write": (_I, [_I, _SZ, _SZ, _SZ, _U16P, _U16P, _SZ, _U8P, _SZ]),
     "amsq_container_read": (_I, [_U8P, _SZ, C.POINTER(C.c_int), C.POINTER(_SZ), C.POINTER(_SZ),

@@ -485,6 +485,47 @@ int amsq_quantize_device(int id, const float* d_w, size_t rows, size_t cols, siz
   });
 }
 
+int amsq_quantize_device_host(int id, size_t rows, size_t cols, const float* w, int device,
+                              size_t* padded, size_t* words, uint16_t* scales, uint16_t* payload) {
+  return guarded([&] {
+    const amsqb::Scheme& s = amsqb::scheme(id);
+    if (rows == 0 || cols == 0) throw amsqb::InvalidArgument("quantize_tensor: empty matrix");
+    const size_t pc = amsqb::padded_cols(s, cols), nw = rows * amsqb::words_per_row(s, pc);
+    if (padded) *padded = pc;
+    if (words) *words = nw;
+    if (!scales && !payload) return;
+    if (!scales || !payload || !w) throw amsqb::InvalidArgument("quantize_tensor: null buffer");
+    require_device(device);
+    DeviceGuard dg(device);
+    // stream-ordered scratch on a private stream: w in, scales + payload out (synchronous call)
+    cudaStream_t st = nullptr;
+    ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    struct StreamGone {
+      cudaStream_t s;
+      ~StreamGone() { cudaStreamDestroy(s); }
+    } gone{st};
+    const size_t wb = (rows * cols * sizeof(float) + 255) / 256 * 256, sb = (rows * 2 + 255) / 256 * 256;
+    void* d = nullptr;
+    ck(cudaMallocAsync(&d, wb + sb + nw * 2, st), "cudaMallocAsync(quantize)");
+    auto* dw = static_cast<float*>(d);
+    auto* ds = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(d) + wb);
+    auto* dp = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(d) + wb + sb);
+    ck(cudaMemcpyAsync(dw, w, rows * cols * sizeof(float), cudaMemcpyHostToDevice, st), "H2D w");
+    const int rc = amsq_quantize_device(id, dw, rows, cols, cols, ds, dp, nw, device, st);
+    if (rc != AMSQ_OK) {
+      const std::string msg = g_error;
+      cudaFreeAsync(d, st);
+      cudaStreamSynchronize(st);
+      if (rc == AMSQ_ECORRUPT) throw amsqb::Corrupt(msg);
+      throw amsqb::InvalidArgument(msg);
+    }
+    ck(cudaMemcpyAsync(scales, ds, rows * 2, cudaMemcpyDeviceToHost, st), "D2H scales");
+    ck(cudaMemcpyAsync(payload, dp, nw * 2, cudaMemcpyDeviceToHost, st), "D2H payload");
+    ck(cudaFreeAsync(d, st), "cudaFreeAsync(quantize)");
+    ck(cudaStreamSynchronize(st), "quantize sync");
+  });
+}
+
 int amsq_container_size(int id, size_t rows, size_t cols, size_t* bytes) {
   return guarded([&] { *bytes = amsqb::container_bytes(amsqb::scheme(id), rows, cols); });
 }

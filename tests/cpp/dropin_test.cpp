@@ -115,6 +115,26 @@ void gpu_suite() {
   report("gemv batch 0 -> invalid_argument", throws<std::invalid_argument>([&] {
            amsq_b200::gemv(qt, std::vector<uint16_t>(9, 0), 0);
          }));
+  // quantize.hpp:188-216 on the GPU: the reference's own quantize_tensor, bit for bit
+  for (const char* name : {"fp5.33-e2m3", "fp4.25-e2m2", "fp6-e3m2", "fp4-e2m1"}) {
+    const amsq::QuantScheme& s = amsq::scheme_by_name(name);
+    for (auto [rows, cols] : {std::pair<size_t, size_t>{7, 50}, {64, 192}, {300, 4098}}) {
+      const amsq::Matrix w = amsq::detail::gaussian_matrix(rows, cols, 3 * rows + cols);
+      const auto ref = amsq::quantize_tensor(w, s);
+      const auto dev = amsq_b200::quantize_tensor<amsq::QuantizedTensor>(w, s);
+      report(std::string("quantize_tensor on the GPU bit-exact ") + name + " " + std::to_string(rows) +
+                 "x" + std::to_string(cols),
+             dev.padded_cols == ref.padded_cols && dev.scales == ref.scales && dev.payload == ref.payload);
+    }
+  }
+  {
+    amsq::Matrix bad = amsq::detail::gaussian_matrix(3, 8, 2);
+    bad.data[5] = std::nanf("");
+    report("quantize_tensor non-finite -> runtime_error (quantize.hpp:77)",
+           throws<std::runtime_error>([&] {
+             amsq_b200::quantize_tensor<amsq::QuantizedTensor>(bad, amsq::scheme_by_name("fp5.33-e2m3"));
+           }));
+  }
   // resident weights: download is the reference stream, bit for bit
   amsq_b200::DeviceTensor t(qt);
   std::vector<uint16_t> sc, pl;
@@ -132,6 +152,11 @@ void no_gpu_suite() {
          throws<std::runtime_error>([&] { amsq_b200::restore_matrix_half(qt); }));
   report("gemv shape mismatch -> invalid_argument (before any device work)",
          throws<std::invalid_argument>([&] { amsq_b200::gemv(qt, x, 2); }));
+  report("quantize_tensor without a GPU -> runtime_error (no CPU fallback)",
+         throws<std::runtime_error>([&] {
+           amsq_b200::quantize_tensor<amsq::QuantizedTensor>(amsq::detail::gaussian_matrix(4, 9, 1),
+                                                             amsq::scheme_by_name("fp5.33-e2m3"));
+         }));
 }
 
 }  // namespace

@@ -341,3 +341,20 @@ def test_k2_k3_dispatch_crossover():
     assert prev == -1 and L.amsq_linear_uses_tc(4, 17) == 1 and L.amsq_linear_uses_tc(7, 16) == 0
     assert L.amsq_debug_set_k3_min_batch(prev) == 17
     assert L.amsq_linear_uses_tc(7, 47) == 0 and L.amsq_linear_uses_tc(4, 64) == 0
+
+
+def test_quantize_device_host_query_and_errors():
+    """amsq_quantize_device_host: the size query works without a device (as amsq_quantize_tensor's
+    does); argument errors are EINVAL; a real call without a GPU is ENODEV (no host fallback)."""
+    from paper_2510_16045_b200._lib import AMSQ_EINVAL, AMSQ_ENODEV
+    import torch
+    pc, nw = C.c_size_t(0), C.c_size_t(0)
+    assert lib().amsq_quantize_device_host(7, 5, 10, None, 0, C.byref(pc), C.byref(nw), None, None) == 0
+    assert (pc.value, nw.value) == (12, 5 * 4)
+    assert lib().amsq_quantize_device_host(7, 0, 10, None, 0, C.byref(pc), C.byref(nw), None, None) == AMSQ_EINVAL
+    if not torch.cuda.is_available():
+        w = np.ones((5, 10), np.float32)
+        sc = np.zeros(5, np.uint16)
+        pl = np.zeros(20, np.uint16)
+        assert lib().amsq_quantize_device_host(7, 5, 10, w.ctypes.data, 0, C.byref(pc), C.byref(nw),
+                                               sc.ctypes.data, pl.ctypes.data) == AMSQ_ENODEV
