@@ -277,6 +277,10 @@ void amsq_debug_set_trace(void* d_buf);
  * (FP5.33: 48, FP4.25: 65), rows < 0 restores it, 0 only queries. Returns the previous setting
  * (-1 = the per-scheme defaults). Process-wide. */
 int amsq_debug_set_k3_min_batch(int rows);
+/* K3 CTA-pair knob (cta_group::2 M = 256 MMAs, the activation image split across the pair):
+ * -1 the measured rule (FP5.33 at 113..128 batch rows), 0 never, 1 whenever K is not split across
+ * a cluster. Returns the previous setting. Test / tuning use. */
+int amsq_debug_set_k3_pair(int mode);
 /* 1 when amsq_linear on a batch of `batch` rows of this scheme runs K3 (tcgen05), 0 for K2. */
 int amsq_linear_uses_tc(int scheme_id, size_t batch);
 

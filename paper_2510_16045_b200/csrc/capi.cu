@@ -1131,4 +1131,6 @@ int amsq_debug_set_k3_min_batch(int rows) {
 
 int amsq_linear_uses_tc(int scheme_id, size_t batch) { return uses_k3(scheme_id, batch) ? 1 : 0; }
 
+int amsq_debug_set_k3_pair(int mode) { return amsqb::tc_set_pair_knob(mode); }
+
 }  // extern "C"

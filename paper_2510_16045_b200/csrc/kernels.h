@@ -108,6 +108,9 @@ cudaError_t launch_quantize(const QuantTables& tb, const float* w, long long row
 cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
                              long long cols, cudaStream_t s);
 constexpr int kTcMaxBatch = 256;
+// K3 CTA-pair mode (cta_group::2): -1 = the measured rule, 0 = never, 1 = whenever no K split is
+// chosen and there are >= 2 row blocks. Returns the previous setting.
+int tc_set_pair_knob(int v);
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
 // Fused-TP flag barrier (one tiny launch per call): publish epoch e = *epoch + 1 into every
 // rank's flag array at index `rank`, wait until all ranks published e here, then *epoch = e.

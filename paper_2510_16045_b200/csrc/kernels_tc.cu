@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 
@@ -67,10 +68,11 @@ __device__ __forceinline__ int tc_kperm(int p) {
 }
 
 // x[M][ldx] -> xk[KTOT/8][Np][8] (the UMMA no-swizzle K-major image), K permuted per tile.
+// nh = 2 (CTA pairs): two images [2][KTOT/8][Np/2][8], one per CTA of a pair (its N half).
 template <int SCHEME>
 __global__ void __launch_bounds__(256) amsq_xprep_tc_kernel(const unsigned short* __restrict__ x,
                                                             long long ldx, long long cols, int M,
-                                                            int Np, int KT,
+                                                            int Np, int KT, int nh,
                                                             unsigned short* __restrict__ xk) {
   constexpr int TK = Traits<SCHEME>::kTK;
   pdl_launch_dependents();
@@ -78,9 +80,13 @@ __global__ void __launch_bounds__(256) amsq_xprep_tc_kernel(const unsigned short
   const long long total = static_cast<long long>(KT) * TK * Np;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long grp = e / (8LL * Np);
-    const int rem = static_cast<int>(e - grp * 8LL * Np);
-    const int m = rem >> 3, kk = rem & 7;
+    const int Nh = Np / nh;
+    const long long g8 = e / (8LL * Nh);                // (half, k8) flattened
+    const int rem = static_cast<int>(e - g8 * 8LL * Nh);
+    const long long hk = static_cast<long long>(KT) * TK / 8;
+    const int h = static_cast<int>(g8 / hk);
+    const long long grp = g8 - h * hk;
+    const int m = h * Nh + (rem >> 3), kk = rem & 7;
     const long long kp = grp * 8 + kk;                // permuted column
     const long long kt = kp / TK;
     const long long k = kt * TK + tc_kperm<SCHEME>(static_cast<int>(kp - kt * TK));
@@ -183,26 +189,36 @@ __device__ __forceinline__ void tc_cluster_sync() {
 // k-tile. Few large copies keep the bulk engine's per-copy cost off the critical path.
 constexpr int kTcMaxSeg = 8;
 
+// CS = 0: CTA-pair mode (cta_group::2). The two CTAs of a cluster own consecutive 128-row blocks
+// (A and D in their own TMEM) and the two N halves of the activation image (B in their own shared
+// memory); the leader (rank 0) issues M = 256 MMAs over both, the follower's MMA warp relays its
+// stage readiness to the leader, and the leader's commits arrive on both CTAs' barriers. Each SM
+// thus streams half the activation bytes per weight row (tools/pair_probe.cu checked the operand
+// split on the B200).
 template <int SCHEME, int CS>
 __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams p, TcGeom geo) {
+  constexpr bool PAIR = CS == 0;
+  constexpr int KS = PAIR ? 1 : CS;  // CTAs splitting K
   using T = Traits<SCHEME>;
   constexpr int TILE = T::kTileBytes, TK = T::kTK, J = T::kJ;
   constexpr int RUN = SCHEME == 7 ? 12 : 16;  // columns a lane emits per row and tile
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int blk = blockIdx.x / CS;
-  const uint32_t crank = CS > 1 ? tc_cluster_rank() : 0u;
+  const int blk = blockIdx.x / KS;
+  const uint32_t crank = (PAIR || KS > 1) ? tc_cluster_rank() : 0u;  // pair rank or K-split rank
   const int KT = p.k_tiles;
-  const int kper = (KT + CS - 1) / CS;
-  const int kb = static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
+  const int kper = (KT + KS - 1) / KS;
+  const int kb = PAIR ? 0 : static_cast<int>(crank) * kper, ke = min(KT, kb + kper);
   const int nst = ke > kb ? (ke - kb + geo.kchunk - 1) / geo.kchunk : 0;
   uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + geo.stages * geo.stage);
   uint64_t* fullB = fullA + geo.stages;  // activations + weights of the stage landed
   uint64_t* empty = fullB + geo.stages;
   uint64_t* done = empty + geo.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* peer = done + 1;  // pair leader: the follower's stage s is ready (A decoded, B landed)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer + geo.stages);
   int* seg = reinterpret_cast<int*>(tmem_slot + 4);  // [kTcMaxSeg][4]: row0, rows, whole, src tile
-  const uint32_t lboA = 128 * 16, lboB = static_cast<uint32_t>(p.Np) * 16;
+  const int Nh = PAIR ? p.Np / 2 : p.Np;  // activation columns this CTA holds
+  const uint32_t lboA = 128 * 16, lboB = static_cast<uint32_t>(Nh) * 16;
   const int rb0 = blk * 8, rb1 = min(rb0 + 8, p.row_tiles);
   const GroupPlan& P = p.plan;
 
@@ -219,6 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       mbar_init(&fullA[s], kTcDecodeWarps);
       mbar_init(&fullB[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&peer[s], 1);
     }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -240,13 +257,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   }
   __syncwarp();  // reconverge warp 0 before the aligned barriers below
   if (warp == kTcDecodeWarps) {  // TMEM: Np fp32 columns x 128 lanes
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(geo.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(geo.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(geo.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) tc_cluster_sync();  // the peer's barriers and TMEM exist before any remote use
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -402,7 +427,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           }
           wdst += geo.kchunk * n * TILE;
         }
-        bulk_g2s(sp + geo.a_bytes, p.xk + static_cast<long long>(kt0) * TK * p.Np, xbytes,
+        const long long himg = PAIR ? static_cast<long long>(crank) * KT * TK * Nh : 0;  // this CTA's half
+        bulk_g2s(sp + geo.a_bytes, p.xk + himg + static_cast<long long>(kt0) * TK * Nh, xbytes,
                  &fullB[sidx], policy_evict_last());
         if (tr8 && st < 8) trace[16 + st] = clock64();
       }
@@ -414,12 +440,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     // whole warp waits, one thread issues
     const uint32_t idesc = (1u << 4)                                      // D: f32
                            | (static_cast<uint32_t>(p.Np >> 3) << 17)     // N
-                           | (static_cast<uint32_t>(128 >> 4) << 24);     // M
+                           | (static_cast<uint32_t>((PAIR ? 256 : 128) >> 4) << 24);  // M
     int sidx = 0;
     uint32_t ph = 0;
+    if (PAIR && crank != 0) {
+      // follower: relay each stage's readiness (A decoded into this CTA's TMEM, B half landed)
+      // to the leader, which issues the pair's MMAs
+      uint32_t lead_peer;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_peer) : "r"(smem_u32(peer)));
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(&fullA[sidx], ph);
+        mbar_wait(&fullB[sidx], ph);
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(lead_peer + sidx * 8)
+                       : "memory");
+        }
+        __syncwarp();
+        if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+      }
+    } else
     for (int st = 0; st < nst; ++st) {
       mbar_wait(&fullA[sidx], ph);
       mbar_wait(&fullB[sidx], ph);
+      if constexpr (PAIR) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WPEER_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WPEER_%=;\n}" ::"r"(smem_u32(&peer[sidx])),
+            "r"(ph)
+            : "memory");
+      }
       tc_fence_after();
       if (tr8 && lane == 0 && st < 8) trace[40 + st] = clock64();
       if (lane == 0) {
@@ -430,19 +481,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
           const uint64_t bd = umma_desc(b0 + k16 * 2 * lboB, lboB, 128);
 #if AMSQ_TC_ATMEM
           const uint32_t at = tmem + static_cast<uint32_t>(geo.a_col0 + sidx * geo.cols_a + k16 * 8);
-          tc_mma_f16_ts(tmem, at, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+          if constexpr (PAIR) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                "r"(at), "l"(bd), "r"(idesc), "r"((st > 0 || k16 > 0) ? 1u : 0u)
+                : "memory");
+          } else {
+            tc_mma_f16_ts(tmem, at, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+          }
 #else
           const uint64_t ad = umma_desc(a0 + k16 * 2 * lboA, lboA, 128);
           tc_mma_f16(tmem, ad, bd, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
 #endif
         }
-        tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
+        if constexpr (PAIR) {  // both CTAs' stage s: their A (TMEM) and B halves were read
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[sidx])),
+              "h"(static_cast<uint16_t>(3))
+              : "memory");
+        } else {
+          tc_commit(&empty[sidx]);  // frees the stage once these MMAs have read it
+        }
         if (tr8 && st < 8) trace[48 + st] = clock64();
       }
       __syncwarp();
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
     }
-    if (lane == 0) tc_commit(done);
+    if (lane == 0 && !(PAIR && crank != 0)) {
+      if constexpr (PAIR) {
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(done)),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+      } else {
+        tc_commit(done);
+      }
+    }
     __syncwarp();
   }
 
@@ -451,7 +528,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
   const long long n = static_cast<long long>(blk) * 128 + row;
-  const int nchunks = p.Np / 16, ncap = (nchunks + CS - 1) / CS * 16;  // owned columns / rank
+  const int nchunks = p.Np / 16, ncap = (nchunks + KS - 1) / KS * 16;  // owned columns / rank
   const int nch_half = (nchunks + 1) / 2;  // 16-column chunks per epilogue warp half
   float* recv = reinterpret_cast<float*>(smem);  // [CS][ncap][128] (the idle stage ring)
   auto store_y = [&](int m, float v) {
@@ -465,7 +542,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
     tc_fence_after();
   }
   if (trace && threadIdx.x == 0) trace[2] = globaltimer();
-  if constexpr (CS > 1) {
+  if constexpr (KS > 1) {
     // every rank's MMAs have finished reading its stage ring before any rank writes partials
     // into a peer's (reused) ring
     __syncwarp();
@@ -485,11 +562,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K range: a zero partial
       }
-      if constexpr (CS == 1) {
+      if constexpr (KS == 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) store_y(c0 + j, __uint_as_float(v[j]));
       } else {
-        const int owner = ci % CS, slot = (ci / CS) * 16;
+        const int owner = ci % KS, slot = (ci / KS) * 16;
         // [rank][column][row]: consecutive lanes (rows) hit consecutive banks
         float* dst = recv + (static_cast<long long>(crank) * ncap + slot) * 128 + row;
         uint32_t remote;
@@ -502,7 +579,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       }
     }
   }
-  if constexpr (CS > 1) {
+  if constexpr (KS > 1) {
     __syncwarp();
     tc_fence_before();
     tc_cluster_sync();  // all remote partials have landed
@@ -510,13 +587,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
       pdl_wait();
       for (int ci = half * nch_half; ci < min(nchunks, (half + 1) * nch_half); ++ci) {
         const int c0 = ci * 16;
-        if (ci % CS != static_cast<int>(crank)) continue;
-        const int slot = (ci / CS) * 16;
+        if (ci % KS != static_cast<int>(crank)) continue;
+        const int slot = (ci / KS) * 16;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float v = 0.0f;
 #pragma unroll
-          for (int r = 0; r < CS; ++r) v += recv[(static_cast<long long>(r) * ncap + slot + j) * 128 + row];
+          for (int r = 0; r < KS; ++r) v += recv[(static_cast<long long>(r) * ncap + slot + j) * 128 + row];
           store_y(c0 + j, v);  // rank order: deterministic
         }
       }
@@ -526,7 +603,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) amsq_linear_tc_kernel(TcParams 
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (warp == kTcDecodeWarps) {
+  if constexpr (PAIR) {
+    tc_cluster_sync();  // the leader's MMAs wrote this CTA's TMEM; both are done with it
+    if (warp == kTcDecodeWarps) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(geo.tmem_cols));
+    }
+  } else if (warp == kTcDecodeWarps) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(geo.tmem_cols));
   }
@@ -544,7 +627,7 @@ static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int sm
     return e;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(rb * CS));
+  cfg.gridDim = dim3(static_cast<unsigned>(CS == 0 ? (rb + 1) / 2 * 2 : rb * CS));  // CS = 0: CTA pairs
   cfg.blockDim = dim3(dev::kTcThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = s;
@@ -552,9 +635,9 @@ static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int sm
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   int na = 1;
-  if constexpr (CS > 1) {
+  if constexpr (CS != 1) {
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = CS;
+    attr[1].val.clusterDim.x = CS == 0 ? 2 : CS;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     na = 2;
@@ -566,11 +649,61 @@ static cudaError_t launch_tc_m(const TcParams& p, const dev::TcGeom& geo, int sm
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+int tc_pair_knob();
+
 template <int SCHEME>
 static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long long ldx,
                                long long cols, cudaStream_t s) {
   using T = dev::Traits<SCHEME>;
-  // activation prep (PDL-chained)
+  // stage geometry for an activation image of nb columns per CTA
+  auto geometry = [&](int nb) {
+    dev::TcGeom geo{}, best{};
+    best.stages = 0;
+    const int budget = 227 * 1024 - 2048;
+    for (int kc : {4, 2}) {  // k-tiles per stage (even: two decode warps per row tile)
+      geo.kchunk = kc;
+      geo.a_bytes = AMSQ_TC_ATMEM ? 0 : 128 * kc * T::kTK * 2;
+      geo.b_bytes = nb * kc * T::kTK * 2;
+      geo.stage = (geo.a_bytes + geo.b_bytes + 8 * kc * T::kTileBytes + 1023) / 1024 * 1024;
+      geo.stages = budget / geo.stage;
+      if (AMSQ_TC_ATMEM) {  // the A ring shares TMEM with the Np accumulator columns
+        geo.a_col0 = p.Np <= 128 ? 128 : 256;
+        geo.cols_a = kc * T::kTK / 2;
+        geo.stages = std::min(geo.stages, (512 - geo.a_col0) / geo.cols_a);
+      }
+      if (geo.stages >= 4 || geo.stages > best.stages) best = geo;
+      if (geo.stages >= 4) break;
+    }
+    geo = best;
+    if (geo.stages > (AMSQ_TC_ATMEM ? 8 : 6)) geo.stages = AMSQ_TC_ATMEM ? 8 : 6;
+    geo.tmem_cols = 32;
+    while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
+    if (AMSQ_TC_ATMEM) geo.tmem_cols = 512;
+    return geo;
+  };
+  dev::TcGeom geo = geometry(p.Np);
+  if (geo.stages < 2) return cudaErrorInvalidConfiguration;
+  // split K over a cluster when the 128-row blocks alone leave SMs idle
+  const int rb = (p.row_tiles + 7) / 8;
+  int cs = 1;
+  while (cs < 4 && rb * cs * 2 <= 148 && p.k_tiles >= 8 * cs * 2 &&
+         (cs * 2 != 4 || rb <= 32)) {
+    cs *= 2;
+  }
+  const int nchunks = p.Np / 16;
+  const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
+  if (cs > 1 && geo.stages * geo.stage < recv) cs = 1;
+  // otherwise CTA pairs (cta_group::2, M = 256): each CTA streams half the activation image. The
+  // pair's per-stage handshake pays off only for large stages full of activations: measured 1.25x
+  // at 128 batch rows where the halved image admits 4 k-tiles per stage (the single CTA then runs 2),
+  // 4-7 % slower elsewhere (profiles/r02/k3_pair_ab.txt)
+  const int knob = tc_pair_knob();
+  const dev::TcGeom pgeo = geometry(p.Np / 2);  // halving the image lets a pair take bigger stages
+  const bool pair_ok = AMSQ_TC_ATMEM && cs == 1 && rb >= 2 && pgeo.stages >= 2;
+  const bool pair = pair_ok && (knob == 1 || (knob < 0 && pgeo.kchunk == 4 && p.Np >= 128));
+  if (pair) geo = pgeo;
+  const int smem = geo.stages * geo.stage + (4 * geo.stages + 1) * 8 + 16 + dev::kTcMaxSeg * 16;
+  // activation prep (PDL-chained): one image, or the two N halves of a pair
   {
     const long long total = static_cast<long long>(p.k_tiles) * T::kTK * p.Np;
     cudaLaunchConfig_t cfg{};
@@ -583,50 +716,21 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, dev::amsq_xprep_tc_kernel<SCHEME>, x, ldx, cols, p.M,
-                                       p.Np, p.k_tiles, const_cast<unsigned short*>(p.xk));
+                                       p.Np, p.k_tiles, pair ? 2 : 1, const_cast<unsigned short*>(p.xk));
     count_launch();
     if (e != cudaSuccess) return e;
   }
-  dev::TcGeom geo{}, best{};
-  best.stages = 0;
-  const int budget = 227 * 1024 - 2048;
-  for (int kc : {4, 2}) {  // k-tiles per stage (even: two decode warps per row tile)
-    geo.kchunk = kc;
-    geo.a_bytes = AMSQ_TC_ATMEM ? 0 : 128 * kc * T::kTK * 2;
-    geo.b_bytes = p.Np * kc * T::kTK * 2;
-    geo.stage = (geo.a_bytes + geo.b_bytes + 8 * kc * T::kTileBytes + 1023) / 1024 * 1024;
-    geo.stages = budget / geo.stage;
-    if (AMSQ_TC_ATMEM) {  // the A ring shares TMEM with the Np accumulator columns
-      geo.a_col0 = p.Np <= 128 ? 128 : 256;
-      geo.cols_a = kc * T::kTK / 2;
-      geo.stages = std::min(geo.stages, (512 - geo.a_col0) / geo.cols_a);
-    }
-    if (geo.stages >= 4 || geo.stages > best.stages) best = geo;
-    if (geo.stages >= 4) break;
-  }
-  geo = best;
-  if (geo.stages > (AMSQ_TC_ATMEM ? 8 : 6)) geo.stages = AMSQ_TC_ATMEM ? 8 : 6;
-  if (geo.stages < 2) return cudaErrorInvalidConfiguration;
-  geo.tmem_cols = 32;
-  while (geo.tmem_cols < p.Np) geo.tmem_cols *= 2;
-  if (AMSQ_TC_ATMEM) geo.tmem_cols = 512;
-  const int smem = geo.stages * geo.stage + (3 * geo.stages + 1) * 8 + 16 + dev::kTcMaxSeg * 16;
-  // split K over a cluster when the 128-row blocks alone leave SMs idle
-  const int rb = (p.row_tiles + 7) / 8;
-  int cs = 1;
-  while (cs < 4 && rb * cs * 2 <= 148 && p.k_tiles >= 8 * cs * 2 &&
-         (cs * 2 != 4 || rb <= 32)) {
-    cs *= 2;
-  }
-  const int nchunks = p.Np / 16;
-  const long long recv = static_cast<long long>(cs) * 128 * ((nchunks + cs - 1) / cs * 16) * 4;
-  if (cs > 1 && geo.stages * geo.stage < recv) cs = 1;
+  if (pair) return launch_tc_m<SCHEME, 0>(p, geo, smem, rb, s);
   switch (cs) {
     case 2: return launch_tc_m<SCHEME, 2>(p, geo, smem, rb, s);
     case 4: return launch_tc_m<SCHEME, 4>(p, geo, smem, rb, s);
     default: return launch_tc_m<SCHEME, 1>(p, geo, smem, rb, s);
   }
 }
+
+static std::atomic<int> g_tc_pair{-1};
+int tc_pair_knob() { return g_tc_pair.load(std::memory_order_relaxed); }
+int tc_set_pair_knob(int v) { return g_tc_pair.exchange(v < 0 ? -1 : (v ? 1 : 0)); }
 
 cudaError_t launch_linear_tc(const TcParams& p, const unsigned short* x, long long ldx,
                              long long cols, cudaStream_t s) {

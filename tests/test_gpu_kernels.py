@@ -260,6 +260,31 @@ def test_linear_tcgen05_small_batch(cuda, orc, sid, shape, batch, force_k3_all):
     check_linear(y, yref, yabs)
 
 
+@pytest.fixture
+def force_pairs():
+    from paper_2510_16045_b200._lib import lib
+    prev = lib().amsq_debug_set_k3_pair(1)
+    yield
+    lib().amsq_debug_set_k3_pair(prev)
+
+
+@pytest.mark.parametrize("sid", AMS)
+@pytest.mark.parametrize("rows", [19032, 19200])
+@pytest.mark.parametrize("batch", [17, 64, 128, 200])
+def test_linear_tcgen05_cta_pairs(cuda, orc, sid, rows, batch, force_k3, force_pairs):
+    """K3 in CTA-pair mode (cta_group::2, M = 256 MMAs over two CTAs' 128-row blocks, the
+    activation image split by N across the pair), forced at every batch: 149 row blocks (an odd
+    count: the last pair's follower has no rows) and 150."""
+    cols = 256
+    qt = quantized_gaussian(sid, rows, cols, seed=rows + batch)
+    x = gaussian_x(batch, cols, seed=batch + 5)
+    xt = torch.from_numpy(x.view(np.float16).reshape(batch, cols)).to(cuda)
+    y = amsq.DeviceWeight(qt).linear(xt).cpu().numpy().view(np.uint16).reshape(batch, rows)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y, yref, yabs)
+
+
 @pytest.mark.parametrize("sid", AMS)
 @pytest.mark.parametrize("batch", [17, 48, 112, 144, 200])
 def test_linear_tcgen05_cluster_split_odd_chunks(cuda, orc, sid, batch, force_k3):
