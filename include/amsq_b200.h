@@ -274,11 +274,11 @@ uint64_t amsq_kernel_launch_count(void);
 void amsq_debug_set_trace(void* d_buf);
 /* Dispatch knob: batches of >= rows run the tcgen05 kernel (K3, schemes 4 and 7), smaller ones
  * the mma.sync kernel (K2) in 32-row chunks. rows > 0 overrides the per-scheme measured crossover
- * (FP5.33: 48, FP4.25: 65), rows < 0 restores it, 0 only queries. Returns the previous setting
+ * (FP5.33: 33, FP4.25: 40), rows < 0 restores it, 0 only queries. Returns the previous setting
  * (-1 = the per-scheme defaults). Process-wide. */
 int amsq_debug_set_k3_min_batch(int rows);
 /* K3 CTA-pair knob (cta_group::2 M = 256 MMAs, the activation image split across the pair):
- * -1 the measured rule (FP5.33 at 113..128 batch rows), 0 never, 1 whenever K is not split across
+ * -1 the measured rule (128 batch rows when the halved image admits >= 4 k-tiles per stage), 0 never, 1 whenever K is not split across
  * a cluster. Returns the previous setting. Test / tuning use. */
 int amsq_debug_set_k3_pair(int mode);
 /* 1 when amsq_linear on a batch of `batch` rows of this scheme runs K3 (tcgen05), 0 for K2. */

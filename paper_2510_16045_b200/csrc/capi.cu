@@ -60,12 +60,12 @@ unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA times
 std::atomic<int> g_k3_min_batch{-1};  // > 0: a process-wide override of k3_min_batch()
 
 // Batches of at least this many rows run K3 (tcgen05), smaller ones K2 in 32-row chunks: the
-// measured crossover per scheme (profiles/r02/k3_small_m.txt: with the A operand in TMEM, K3 wins
-// FP5.33 from M = 48 on; FP4.25's gate_up still prefers two K2 launches at M = 64).
+// measured crossover per scheme (profiles/r02/k3_crossover_final.txt, K3 with A in TMEM, 2-8
+// k-tiles per stage and CTA pairs): K3 wins FP5.33 from M = 33 (past one K2 launch), FP4.25 from 40.
 int k3_min_batch(int scheme_id) {
   const int v = g_k3_min_batch.load(std::memory_order_relaxed);
   if (v > 0) return v;
-  return scheme_id == 7 ? 48 : 65;
+  return scheme_id == 7 ? 33 : 40;
 }
 bool uses_k3(int scheme_id, size_t batch) {
   return (scheme_id == 4 || scheme_id == 7) && batch >= static_cast<size_t>(k3_min_batch(scheme_id));

@@ -36,6 +36,12 @@ void count_launch();
 
 namespace dev {
 
+#ifndef AMSQ_TC_KC4_MIN_STAGES  // fewest ring stages for which 4 k-tiles per stage are taken
+#define AMSQ_TC_KC4_MIN_STAGES 3
+#endif
+#ifndef AMSQ_TC_BIG_STAGES  // 1: also try 8 and 6 k-tiles per stage (>= 2 stages)
+#define AMSQ_TC_BIG_STAGES 1
+#endif
 #ifndef AMSQ_TC_ATMEM  // 1: the decoded A operand lives in TMEM (tcgen05.st); 0: shared memory
 #define AMSQ_TC_ATMEM 1
 #endif
@@ -660,7 +666,13 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
     dev::TcGeom geo{}, best{};
     best.stages = 0;
     const int budget = 227 * 1024 - 2048;
-    for (int kc : {4, 2}) {  // k-tiles per stage (even: two decode warps per row tile)
+    // k-tiles per stage (even: two decode warps per row tile): the largest that leaves enough
+    // stages -- per-stage synchronisation, not ring depth, is what K3 pays for
+#if AMSQ_TC_BIG_STAGES
+    for (int kc : {8, 6, 4, 2}) {
+#else
+    for (int kc : {4, 2}) {
+#endif
       geo.kchunk = kc;
       geo.a_bytes = AMSQ_TC_ATMEM ? 0 : 128 * kc * T::kTK * 2;
       geo.b_bytes = nb * kc * T::kTK * 2;
@@ -671,8 +683,9 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
         geo.cols_a = kc * T::kTK / 2;
         geo.stages = std::min(geo.stages, (512 - geo.a_col0) / geo.cols_a);
       }
-      if (geo.stages >= 4 || geo.stages > best.stages) best = geo;
-      if (geo.stages >= 4) break;
+      const int need = kc > 4 ? 2 : AMSQ_TC_KC4_MIN_STAGES;
+      if (geo.stages >= need || geo.stages > best.stages) best = geo;
+      if (geo.stages >= need) break;
     }
     geo = best;
     if (geo.stages > (AMSQ_TC_ATMEM ? 8 : 6)) geo.stages = AMSQ_TC_ATMEM ? 8 : 6;
@@ -700,7 +713,7 @@ static cudaError_t launch_tc_t(const TcParams& p, const unsigned short* x, long 
   const int knob = tc_pair_knob();
   const dev::TcGeom pgeo = geometry(p.Np / 2);  // halving the image lets a pair take bigger stages
   const bool pair_ok = AMSQ_TC_ATMEM && cs == 1 && rb >= 2 && pgeo.stages >= 2;
-  const bool pair = pair_ok && (knob == 1 || (knob < 0 && pgeo.kchunk == 4 && p.Np >= 128));
+  const bool pair = pair_ok && (knob == 1 || (knob < 0 && pgeo.kchunk >= 4 && p.Np >= 128));
   if (pair) geo = pgeo;
   const int smem = geo.stages * geo.stage + (4 * geo.stages + 1) * 8 + 16 + dev::kTcMaxSeg * 16;
   // activation prep (PDL-chained): one image, or the two N halves of a pair

@@ -330,17 +330,17 @@ def test_cpp_dropin_without_gpu():
 
 
 def test_k2_k3_dispatch_crossover():
-    """amsq_linear_uses_tc: the measured per-scheme crossover (FP5.33 K3 from 48 rows, FP4.25
-    from 65, the other schemes always K2), the override knob and its restore."""
+    """amsq_linear_uses_tc: the measured per-scheme crossover (FP5.33 K3 from 33 rows, FP4.25
+    from 40, the other schemes always K2), the override knob and its restore."""
     L = lib()
     assert L.amsq_debug_set_k3_min_batch(0) == -1  # defaults in force
-    assert [L.amsq_linear_uses_tc(7, m) for m in (1, 16, 47, 48, 256)] == [0, 0, 0, 1, 1]
-    assert [L.amsq_linear_uses_tc(4, m) for m in (16, 64, 65, 300)] == [0, 0, 1, 1]
+    assert [L.amsq_linear_uses_tc(7, m) for m in (1, 16, 32, 33, 256)] == [0, 0, 0, 1, 1]
+    assert [L.amsq_linear_uses_tc(4, m) for m in (16, 32, 39, 40, 300)] == [0, 0, 0, 1, 1]
     assert L.amsq_linear_uses_tc(2, 1000) == 0
     prev = L.amsq_debug_set_k3_min_batch(17)
     assert prev == -1 and L.amsq_linear_uses_tc(4, 17) == 1 and L.amsq_linear_uses_tc(7, 16) == 0
     assert L.amsq_debug_set_k3_min_batch(prev) == 17
-    assert L.amsq_linear_uses_tc(7, 47) == 0 and L.amsq_linear_uses_tc(4, 64) == 0
+    assert L.amsq_linear_uses_tc(7, 32) == 0 and L.amsq_linear_uses_tc(4, 39) == 0
 
 
 def test_quantize_device_host_query_and_errors():
