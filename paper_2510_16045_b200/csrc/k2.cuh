@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_CONSUMER_PROXY_FENCE  // consumers fence.proxy.async before releasing a stage
 #define AMSQ_CONSUMER_PROXY_FENCE 0
 #endif
+#ifndef AMSQ_K2_PIPE  // issue both k-tiles' fragment loads before decoding the first (kpw = 2)
+#define AMSQ_K2_PIPE 0
+#endif
 #ifndef AMSQ_K2_LEAN
 #define AMSQ_K2_LEAN 0
 #endif
@@ -438,6 +441,41 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     // the warp's kpw k-tiles x NOWN row tiles of a stage, branch-free for a fixed NOWN
     auto consume = [&](const uint8_t* sp, int nk, auto nown_c) {
       constexpr int NOWN = decltype(nown_c)::value;
+#if AMSQ_K2_PIPE
+      // both k-tiles of the warp's k-slot present: issue every shared-memory load of the two
+      // k-tiles first, so the second k-tile's loads land under the first one's decode + MMAs
+      if (geo.kpw == 2 && 2 * ks + 1 < nk) {
+        uint32_t B0[NB][J][2], B1[NB][J][2];
+        Frag<SCHEME> w0[NOWN], w1[NOWN];
+        const uint8_t* tb0 = sp + (2 * ks * G + rl) * TILE;
+        const uint8_t* tb1 = tb0 + G * TILE;
+        load_bfrag<SCHEME, NB>(sp + geo.w_stage, geo, 2 * ks, g, t, B0);
+#pragma unroll
+        for (int i = 0; i < NOWN; ++i) w0[i] = load_frag<SCHEME>(tb0 + i * geo.wr * TILE, lane);
+        load_bfrag<SCHEME, NB>(sp + geo.w_stage, geo, 2 * ks + 1, g, t, B1);
+#pragma unroll
+        for (int i = 0; i < NOWN; ++i) w1[i] = load_frag<SCHEME>(tb1 + i * geo.wr * TILE, lane);
+#pragma unroll
+        for (int i = 0; i < NOWN; ++i) {
+          uint32_t A[J][4];
+          decode_frag<SCHEME>(w0[i], A);
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) mma16816(acc[i][nb], A[j], B0[nb][j][0], B0[nb][j][1]);
+        }
+#pragma unroll
+        for (int i = 0; i < NOWN; ++i) {
+          uint32_t A[J][4];
+          decode_frag<SCHEME>(w1[i], A);
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) mma16816(acc[i][nb], A[j], B1[nb][j][0], B1[nb][j][1]);
+        }
+        return;
+      }
+#endif
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
         const int kq = geo.kpw * ks + kk;

@@ -203,6 +203,7 @@ def test_tp_fused_epilogue_matches_reference_and_nccl_path(cuda, orc, sid, P):
     at different arena offsets exercise the device-side epochs."""
     from helpers import check_linear, gaussian_x, random_payload
     from paper_2510_16045_b200 import DeviceWeight
+    from paper_2510_16045_b200._lib import lib
     ndev = torch.cuda.device_count()
     devices = [r % ndev for r in range(P)]
     n_local, cols = 512, 4096
@@ -228,7 +229,13 @@ def test_tp_fused_epilogue_matches_reference_and_nccl_path(cuda, orc, sid, P):
                     .reshape(batch, rows).cpu() for r in range(P)]
             for r in range(1, P):
                 assert torch.equal(outs[r], outs[0]), f"rank {r} differs"
-            local = torch.cat([shards[r].linear(xs[r]).cpu() for r in range(P)], dim=1)
+            # the fused epilogue is a K2 epilogue at every batch: compare with the per-shard
+            # K2 outputs even where the dispatch would pick K3 (batch 40 >= the crossover)
+            prev = lib().amsq_debug_set_k3_min_batch(100000)
+            try:
+                local = torch.cat([shards[r].linear(xs[r]).cpu() for r in range(P)], dim=1)
+            finally:
+                lib().amsq_debug_set_k3_min_batch(prev)
             assert torch.equal(outs[0], local)
             yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
             _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x,

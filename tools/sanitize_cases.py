@@ -28,6 +28,7 @@ CASES = [  # (scheme, rows, cols, batch, k3)
     (4, 512, 2048, 48, True),      # K3 tcgen05, 2-CTA split-K
     (7, 1024, 4096, 5, True),      # K3 with one 16-column N chunk (A in TMEM, M < 16)
     (7, 2048, 2048, 128, True),    # K3 C=1, 8 N chunks
+    (7, 4096, 4096, 64, "pair"),   # K3 CTA pair (cta_group::2, M = 256), forced
 ]
 
 
@@ -37,6 +38,7 @@ def main():
     for i in only:
         sid, rows, cols, batch, k3 = CASES[i]
         prev = lib().amsq_debug_set_k3_min_batch(1 if k3 else 100000)
+        prev_pair = lib().amsq_debug_set_k3_pair(1 if k3 == "pair" else -1)
         qt = random_payload(sid, rows, cols, seed=i)
         dw = amsq.DeviceWeight(qt)
         x = gaussian_x(batch, cols, seed=i)
@@ -46,8 +48,9 @@ def main():
         _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
         rel = check_linear(y, yref, yabs)
         lib().amsq_debug_set_k3_min_batch(prev)
+        lib().amsq_debug_set_k3_pair(prev_pair)
         info = dw.info()
-        print(f"case {i}: scheme {sid} {rows}x{cols} M={batch} {'K3' if k3 else 'K2'} "
+        print(f"case {i}: scheme {sid} {rows}x{cols} M={batch} {'K3 pair' if k3 == 'pair' else 'K3' if k3 else 'K2'} "
               f"plan G={info.g_big} C={info.csplit}: rel {rel:.2e} OK", flush=True)
         dw.free()
 
