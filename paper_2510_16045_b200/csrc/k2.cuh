@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
 #define AMSQ_K2_MODE 0  // 2 = decode without MMA, 3 = MMA without decode, 4 = consume without copies
 #endif
 constexpr int kConsumerWarps = AMSQ_K2_WARPS;
-constexpr bool kK2XPrep = AMSQ_K2_XPREP != 0;
+constexpr bool kK2XStage = AMSQ_K2_XSTAGE != 0;
+// the separate prep kernel only when the producer does not permute the activations itself
+constexpr bool kK2XPrep = AMSQ_K2_XPREP != 0 && !kK2XStage;
 constexpr int kK2Threads = (kConsumerWarps + 1) * 32;  // + the producer warp
 #ifndef AMSQ_MAX_OWN1  // row tiles a consumer warp may own at M <= 8 (4 or 8)
 #define AMSQ_MAX_OWN1 4
@@ -147,6 +149,7 @@ struct K2Geom {
   int recv_off;      // byte offset of the cluster reduction's receive buffer
   int recv_in_ring;  // 1: it overlaps the ring, so peers may only store after a cluster barrier
   int bar_off;       // byte offset of the mbarriers (then the staged scales)
+  int xnat_off;      // AMSQ_K2_XSTAGE: natural activation rows, from the stage's activation area
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -166,7 +169,7 @@ __device__ __forceinline__ void load_bfrag(const uint8_t* xs, const K2Geom& geo,
   constexpr int J = T::kJ, MS = 8 * NB;
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    if constexpr (kK2XPrep && NB >= 2) {
+    if constexpr ((kK2XPrep && NB >= 2) || kK2XStage) {
       const uint2* xu = reinterpret_cast<const uint2*>(xs) + ((ks * J) * MS + nb * 8 + g) * 4 + t;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
@@ -213,7 +216,8 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.bar_off);
   uint64_t* empty = full + geo.stages;
   // the group's row scales (fp32, x 2^14), staged once so the epilogue does not wait on HBM
-  float* sscale = reinterpret_cast<float*>(empty + geo.stages);
+  uint64_t* xland = empty + geo.stages;  // kK2XStage: a stage's natural activation rows landed
+  float* sscale = reinterpret_cast<float*>(empty + geo.stages * (kK2XStage ? 2 : 1));
   unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 64 : nullptr;
   if (trace && threadIdx.x == 0) {
     trace[0] = globaltimer();
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       // after the activations were issued / plain-stored (release of the zero tails)
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], kConsumerWarps);
+      if constexpr (kK2XStage) mbar_init(&xland[s], 1);
     }
     fence_barrier_init();
   }
@@ -294,7 +299,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
       uint32_t xbytes = 0;
       if constexpr (kXPrep) {
         xbytes = static_cast<uint32_t>(n0 + n1) * kXTileBytes;
-      } else {
+      } else if constexpr (!kK2XStage) {
         if (x_bulk) xbytes = static_cast<uint32_t>(p.M) * (xvalid(k0, n0) + (n1 ? xvalid(k1, n1) : 0u));
       }
       // no fence.proxy.async: the empty-barrier acquire already orders the consumers' reads
@@ -329,7 +334,16 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
 #endif
       int k0, n0, k1, n1;
       runs(st, k0, n0, k1, n1);
-      uint8_t* xs = smem + sidx * geo.stage + geo.w_stage;
+      uint8_t* xs = smem + sidx * geo.stage + geo.w_stage + (kK2XStage ? geo.xnat_off : 0);
+      uint64_t* xbar = kK2XStage ? &xland[sidx] : &full[sidx];
+      if constexpr (kK2XStage) {
+        // natural rows land on xland; the permute into B-fragment units arrives on full
+        if (lane == 0) {
+          const uint32_t xb = x_bulk ? static_cast<uint32_t>(p.M) * (xvalid(k0, n0) + (n1 ? xvalid(k1, n1) : 0u)) : 0u;
+          mbar_arrive_expect_tx(xbar, xb);
+        }
+        __syncwarp();
+      }
       if constexpr (kXPrep) {
         if (lane == 0) {
           const uint8_t* xp = reinterpret_cast<const uint8_t*>(p.xperm);
@@ -356,7 +370,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
                   make_uint4(0, 0, 0, 0);
             }
             if (lane < p.M && vb) {
-              bulk_g2s(xs + lane * geo.x_row + off * TK * 2, p.x + lane * p.ldx + kx, vb, &full[sidx],
+              bulk_g2s(xs + lane * geo.x_row + off * TK * 2, p.x + lane * p.ldx + kx, vb, xbar,
                        policy_evict_last());
             }
           } else {  // unaligned activations: plain loads
@@ -370,6 +384,42 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
         }
       }
       __syncwarp();  // the lanes' plain stores happen-before lane 0's release
+      if (!kK2XStage && lane == 0) mbar_arrive(&full[sidx]);
+    };
+    // kK2XStage: once stage st's natural rows landed, the producer warp permutes them into the
+    // B-fragment units the consumers read (what amsq_xprep_kernel writes to global memory):
+    // item (k-tile, batch row m, lane column tt) -> J 8-byte units; rows m >= M are zero
+    auto permute_x = [&](int st, int sidx, uint32_t phase) {
+      mbar_wait(&xland[sidx], phase);
+      const uint8_t* xn = smem + sidx * geo.stage + geo.w_stage + geo.xnat_off;
+      uint2* xf = reinterpret_cast<uint2*>(smem + sidx * geo.stage + geo.w_stage);
+      const int nk = min(S, L - st * S), items = nk * MS * 4;
+      constexpr int LK = T::kLaneK;
+      for (int u = lane; u < items; u += 32) {
+        const int ktl = u / (MS * 4), r = u - ktl * (MS * 4), m = r >> 2, tt = r & 3;
+        uint32_t B[J][2];
+        if (m < p.M) {
+          const uint8_t* src = xn + m * geo.x_row + (ktl * TK + tt * LK) * 2;
+          if constexpr (T::kFam == 4) {
+            const uint4 a = *reinterpret_cast<const uint4*>(src);
+            const uint4 b = *reinterpret_cast<const uint4*>(src + 16);
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            bfrag_s4(w, B);
+          } else {
+            const uint2 a = *reinterpret_cast<const uint2*>(src);
+            const uint2 b = *reinterpret_cast<const uint2*>(src + 8);
+            const uint2 d = *reinterpret_cast<const uint2*>(src + 16);
+            const uint32_t w[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
+            bfrag_s7(w, B);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < J; ++j) B[j][0] = B[j][1] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) xf[((ktl * J + j) * MS + m) * 4 + tt] = make_uint2(B[j][0], B[j][1]);
+      }
+      __syncwarp();  // every lane's units happen-before lane 0's release
       if (lane == 0) mbar_arrive(&full[sidx]);
     };
     // the group's row scales (fp32, x 2^14) for the epilogue, staged after the last copy is
@@ -393,6 +443,11 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     if (trace && lane == 0) trace[4] = clock64();
     int sidx = 0;
     uint32_t ph = 0;
+    // kK2XStage: stage st - 1 is permuted after stage st's copies are issued (its rows are
+    // then in flight behind them) when the ring is deep enough to hide the lag
+    const bool xlag = geo.stages >= 3;
+    int psidx = -1;
+    uint32_t pph = 0;
     for (int st = 0; st < nst; ++st) {
       if (st > 0) {
         if (st >= geo.stages) {
@@ -408,10 +463,22 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
         }
       }
       issue_x(st, sidx);
+      if constexpr (kK2XStage) {
+        if (!xlag) {
+          permute_x(st, sidx, ph);
+        } else {
+          if (psidx >= 0) permute_x(st - 1, psidx, pph);
+          psidx = sidx;
+          pph = ph;
+        }
+      }
 #if AMSQ_TRACE_STAGES
       if (trace && lane == 0 && st < 24) trace[32 + st] = clock64();
 #endif
       if (++sidx == geo.stages) sidx = 0, ph ^= 1u;
+    }
+    if constexpr (kK2XStage) {
+      if (psidx >= 0) permute_x(nst - 1, psidx, pph);
     }
     stage_scales();
     // the next call's first stages into L2 (its CTA j starts on an SM this grid frees): the
@@ -763,7 +830,11 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
     const int x_raw = geo.S * T::kTK * 2;
     geo.x_row = x_raw + ((target - x_raw % 128) + 128) % 128;
     geo.xrows = (dev::kK2XPrep && NB >= 2) ? 8 * NB : p.M;
-    const int x_stage = (dev::kK2XPrep && NB >= 2) ? geo.S * T::kJ * 8 * NB * 4 * 8 : geo.xrows * geo.x_row;
+    const int x_frag = geo.S * T::kJ * 8 * NB * 4 * 8;  // B-fragment units of a stage
+    geo.xnat_off = dev::kK2XStage ? x_frag : 0;        // natural rows behind them
+    const int x_stage = dev::kK2XStage                   ? x_frag + geo.xrows * geo.x_row
+                        : (dev::kK2XPrep && NB >= 2) ? x_frag
+                                                       : geo.xrows * geo.x_row;
     geo.stage = (geo.w_stage + x_stage + 127) / 128 * 128;
     geo.stages = budget / geo.stage;
     if (geo.stages > 6) geo.stages = 6;
@@ -792,7 +863,7 @@ static dev::K2Geom k2_geometry(const LinearParams& p, int* smem_bytes) {
   }
   geo.bar_off = geo.recv_in_ring || recv == 0 ? geo.stages * geo.stage
                                               : static_cast<int>((geo.recv_off + recv + 127) / 128 * 128);
-  *smem_bytes = geo.bar_off + 2 * geo.stages * 8 + G * 16 * 4 + 16;
+  *smem_bytes = geo.bar_off + (dev::kK2XStage ? 3 : 2) * geo.stages * 8 + G * 16 * 4 + 16;
   return geo;
 }
 

@@ -120,6 +120,9 @@ cudaError_t launch_tp_barrier(unsigned int* const* peer_flags, unsigned int* my_
                               unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_unshard(const unsigned short* in, int P, int batch, int n, unsigned short* out,
                            cudaStream_t s);
+#ifndef AMSQ_K2_XSTAGE  // 1: K2's producer warp permutes natural activation rows into B-fragment
+#define AMSQ_K2_XSTAGE 0  // units in shared memory (no prep kernel, no consumer PRMTs)
+#endif
 #ifndef AMSQ_K2_MAX_BATCH  // batch rows per K2 launch: 16 (NB <= 2) or 32 (NB = 4 for 17..32)
 #define AMSQ_K2_MAX_BATCH 32
 #endif
