@@ -211,7 +211,9 @@ int amsq_linear_ex(amsq_weight_t h, const void* d_x, int x_dtype, size_t batch, 
 /* The reference call shape end to end: host x in, host y out (H2D, kernel, D2H on
  * `stream`, synchronous on return). x_len must equal batch*cols. The device copies of x and
  * y live in a grow-only scratch buffer per calling thread and device (reused across calls,
- * never freed); pinned host buffers avoid a staging copy in the driver. */
+ * never freed); pinned host buffers avoid a staging copy in the driver. A page-locked y is
+ * written by the kernel's epilogue directly (no D2H copy); a pageable y goes through the
+ * device scratch and a D2H copy. */
 int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batch, uint16_t* y,
                    void* stream);
 
@@ -281,6 +283,9 @@ int amsq_debug_set_k3_min_batch(int rows);
  * -1 the measured rule (128 batch rows when the halved image admits >= 4 k-tiles per stage), 0 never, 1 whenever K is not split across
  * a cluster. Returns the previous setting. Test / tuning use. */
 int amsq_debug_set_k3_pair(int mode);
+/* amsq_gemv_host into page-locked host y: 1 (default) the epilogue stores into y directly, 0 device
+ * scratch + a D2H copy as for pageable y. Returns the previous setting. Test / tuning use. */
+int amsq_debug_set_host_direct(int on);
 /* 1 when amsq_linear on a batch of `batch` rows of this scheme runs K3 (tcgen05), 0 for K2. */
 int amsq_linear_uses_tc(int scheme_id, size_t batch);
 

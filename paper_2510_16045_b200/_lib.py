@@ -115,6 +115,7 @@ SIGNATURES = {
     "amsq_debug_set_k3_min_batch": (_I, [_I]),
     "amsq_linear_uses_tc": (_I, [_I, _SZ]),
     "amsq_debug_set_k3_pair": (_I, [_I]),
+    "amsq_debug_set_host_direct": (_I, [_I]),
 }
 
 _lib = None

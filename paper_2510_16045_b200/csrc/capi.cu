@@ -57,7 +57,8 @@ thread_local std::string g_error;
 unsigned long long* g_trace = nullptr;  // amsq_debug_set_trace(): per-CTA timestamps
 // batches of at least this many rows run K3 (tcgen05); smaller ones run K2 in chunks of
 // linear_max_batch_per_launch() rows (measured crossover)
-std::atomic<int> g_k3_min_batch{-1};  // > 0: a process-wide override of k3_min_batch()
+std::atomic<int> g_k3_min_batch{-1};
+std::atomic<int> g_host_direct{1};  // amsq_gemv_host: epilogue stores into page-locked host y  // > 0: a process-wide override of k3_min_batch()
 
 // Batches of at least this many rows run K3 (tcgen05), smaller ones K2 in 32-row chunks: the
 // measured crossover per scheme (profiles/r02/k3_crossover_final.txt, K3 with A in TMEM, 2-8
@@ -175,6 +176,17 @@ uint8_t* host_call_scratch(int device, size_t bytes) {
     b.n = bytes;
   }
   return static_cast<uint8_t*>(b.p);
+}
+
+// The device address of page-locked host memory, or nullptr for pageable memory.
+void* host_mapped(void* p) {
+  if (g_host_direct.load(std::memory_order_relaxed) == 0) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // pageable pointers on old drivers: clear the sticky-free error
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
 amsqb::GroupPlan plan_of(const amsqb::DeviceLayout& L) {
@@ -317,7 +329,7 @@ void linear_impl(amsq_weight_t h, const uint16_t* d_x, size_t batch, uint16_t* d
   }
   const size_t step = static_cast<size_t>(amsqb::linear_max_batch_per_launch());
   void* async_ws = nullptr;
-  if (batch > 8) p.xperm = k2_workspace(h, st, &async_ws);
+  if (batch > 8 && !AMSQ_K2_XSTAGE) p.xperm = k2_workspace(h, st, &async_ws);
   for (size_t b0 = 0; b0 < batch; b0 += step) {
     const size_t mb = batch - b0 < step ? batch - b0 : step;
     p.x = reinterpret_cast<const unsigned short*>(d_x) + b0 * h->L.cols;
@@ -833,8 +845,13 @@ int amsq_gemv_host(amsq_weight_t h, const uint16_t* x, size_t x_len, size_t batc
     void* dx = scratch;
     void* dy = scratch + xb;
     ck(cudaMemcpyAsync(dx, x, x_len * 2, cudaMemcpyHostToDevice, st), "H2D x");
-    linear_impl(h, static_cast<const uint16_t*>(dx), batch, static_cast<uint16_t*>(dy), h->L.rows, st);
-    ck(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st), "D2H y");
+    // y in page-locked host memory (cudaHostAlloc / cudaHostRegister, e.g. torch pin_memory):
+    // the epilogue stores each output element straight into it over the host link, which
+    // saves the D2H copy's launch and completion latency. Pageable y: device scratch + D2H.
+    void* hy = host_mapped(y);
+    linear_impl(h, static_cast<const uint16_t*>(dx), batch, static_cast<uint16_t*>(hy ? hy : dy),
+                h->L.rows, st);
+    if (!hy) ck(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st), "D2H y");
     ck(cudaStreamSynchronize(st), "gemv sync");
   });
 }
@@ -1132,5 +1149,7 @@ int amsq_debug_set_k3_min_batch(int rows) {
 int amsq_linear_uses_tc(int scheme_id, size_t batch) { return uses_k3(scheme_id, batch) ? 1 : 0; }
 
 int amsq_debug_set_k3_pair(int mode) { return amsqb::tc_set_pair_knob(mode); }
+
+int amsq_debug_set_host_direct(int on) { return g_host_direct.exchange(on ? 1 : 0); }
 
 }  // extern "C"

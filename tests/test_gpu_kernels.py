@@ -95,6 +95,37 @@ def test_linear_random_payload_large_k(cuda, orc, sid):
     check_linear(y, yref, yabs)
 
 
+@pytest.mark.parametrize("batch", [1, 16, 40, 128])
+@pytest.mark.parametrize("sid", SCHEMES)
+def test_gemv_host_pinned_y_direct(cuda, orc, sid, batch):
+    """amsq_gemv_host into page-locked host y: the epilogue (K2 or K3) stores y over the host
+    link instead of a D2H copy. Bit-identical to the pageable-y path, within the bar."""
+    import torch
+
+    from paper_2510_16045_b200._lib import check, lib
+    rows, cols = 1024, 4096
+    qt = random_payload(sid, rows, cols, seed=batch)
+    x = gaussian_x(batch, cols, seed=batch + 1)
+    dw = amsq.DeviceWeight(qt)
+    y_pageable = dw.gemv_host(x, batch)
+    hy = torch.full((batch * rows,), -1, dtype=torch.int16).pin_memory()
+    hx = torch.from_numpy(x.view(np.int16).copy()).pin_memory()
+    st = torch.cuda.current_stream().cuda_stream
+    check(lib().amsq_gemv_host(dw._h, hx.data_ptr(), x.size, batch, hy.data_ptr(), st), "gemv")
+    y_direct = hy.numpy().view(np.uint16)
+    assert np.array_equal(y_direct, y_pageable)
+    prev = lib().amsq_debug_set_host_direct(0)
+    try:
+        hy.fill_(-1)
+        check(lib().amsq_gemv_host(dw._h, hx.data_ptr(), x.size, batch, hy.data_ptr(), st), "gemv")
+    finally:
+        lib().amsq_debug_set_host_direct(prev)
+    assert np.array_equal(hy.numpy().view(np.uint16), y_pageable)
+    yref = orc.gemv(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    _, yabs = orc.gemv_f64(sid, rows, cols, qt.padded_cols, qt.scales, qt.payload, x, batch)
+    check_linear(y_direct.reshape(batch, rows), yref, yabs)
+
+
 @pytest.mark.parametrize("sid", SCHEMES)
 def test_subnormal_codes_survive_the_tensor_cores(cuda, orc, sid):
     """Placed subnormal-source codes are binary16 subnormals; the MMA must not flush them."""
