@@ -15,7 +15,7 @@ OUT = os.path.join(ROOT, "profiles", sys.argv[1] if len(sys.argv) > 1 else "r01"
 KEEP = ["amsq_linear_kernelILi7ELi1ELi1E", "amsq_linear_kernelILi7ELi1ELi2E",
         "amsq_linear_kernelILi4ELi1ELi2E", "amsq_linear_kernelILi7ELi2ELi2E",
         "amsq_linear_kernelILi7ELi4ELi1E",
-        "amsq_linear_tc_kernelILi7ELi4E", "amsq_linear_tc_kernelILi7ELi1E",
+        "amsq_linear_tc_kernelILi7ELi4E", "amsq_linear_tc_kernelILi7ELi0E", "amsq_linear_tc_kernelILi7ELi1E",
         "amsq_linear_tc_kernelILi4ELi1E", "amsq_restore_kernelILi7E", "amsq_xprep_tc_kernelILi7E",
         "amsq_quantize_kernel"]
 
