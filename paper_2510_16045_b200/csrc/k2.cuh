@@ -24,7 +24,7 @@ namespace dev {
 // row m), zero for m >= M and k >= cols. One thread per (k-tile, row, lane-column) item.
 // =====================================================================================
 template <int SCHEME>
-__global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* __restrict__ x,
+__global__ void __launch_bounds__(128) amsq_xprep_kernel(const unsigned short* __restrict__ x,
                                                          long long ldx, long long cols, int M,
                                                          int MS, int KT, uint2* __restrict__ xp) {
   using T = Traits<SCHEME>;
@@ -36,14 +36,35 @@ __global__ void __launch_bounds__(256) amsq_xprep_kernel(const unsigned short* _
     const int kt = u / (MS * 4), r = u - kt * MS * 4, m = r >> 2, t = r & 3;
     const long long k = static_cast<long long>(kt) * T::kTK + t * LK;
     uint32_t w[LW];
+    const unsigned short* xr = x + m * ldx + k;
+    // the lane's LK columns are one aligned 24-byte (FP5.33 family) or 32-byte run: vector loads
+    // when the row and base alignment allow and the run lies inside `cols`
+    constexpr int VB = LW % 4 == 0 ? 16 : 8;
+    const bool vec = m < M && k + LK <= cols && (reinterpret_cast<uintptr_t>(xr) & (VB - 1)) == 0;
+    if (vec) {
+      if constexpr (VB == 16) {
 #pragma unroll
-    for (int i = 0; i < LW; ++i) {
-      unsigned lo = 0, hi = 0;
-      if (m < M) {
-        if (k + 2 * i < cols) lo = __ldg(x + m * ldx + k + 2 * i);
-        if (k + 2 * i + 1 < cols) hi = __ldg(x + m * ldx + k + 2 * i + 1);
+        for (int i = 0; i < LW; i += 4) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(xr) + i / 4);
+          w[i] = v.x, w[i + 1] = v.y, w[i + 2] = v.z, w[i + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < LW; i += 2) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(xr) + i / 2);
+          w[i] = v.x, w[i + 1] = v.y;
+        }
       }
-      w[i] = lo | hi << 16;
+    } else {
+#pragma unroll
+      for (int i = 0; i < LW; ++i) {
+        unsigned lo = 0, hi = 0;
+        if (m < M) {
+          if (k + 2 * i < cols) lo = __ldg(xr + 2 * i);
+          if (k + 2 * i + 1 < cols) hi = __ldg(xr + 2 * i + 1);
+        }
+        w[i] = lo | hi << 16;
+      }
     }
     uint32_t B[J][2];
     if constexpr (T::kFam == 4) {
@@ -908,8 +929,8 @@ static cudaError_t launch_linear_t(const LinearParams& p, cudaStream_t s) {
     const int MS = 8 * NB;
     const int items = p.k_tiles * MS * 4;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>((items + 255) / 256));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3(static_cast<unsigned>((items + 127) / 128));  // more SMs: latency-bound
+    cfg.blockDim = dim3(128);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
