@@ -127,6 +127,9 @@ __global__ void __launch_bounds__(128) amsq_xprep_kernel(const unsigned short* _
 #ifndef AMSQ_CONSUMER_PROXY_FENCE  // consumers fence.proxy.async before releasing a stage
 #define AMSQ_CONSUMER_PROXY_FENCE 0
 #endif
+#ifndef AMSQ_K2_PRE_W  // ring stages whose weights are requested before griddepcontrol.wait
+#define AMSQ_K2_PRE_W 1
+#endif
 #ifndef AMSQ_K2_PIPE  // issue both k-tiles' fragment loads before decoding the first (kpw = 2)
 #define AMSQ_K2_PIPE 0
 #endif
@@ -456,8 +459,9 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     // stage 0's weights do not depend on the previous kernel: request them before
     // griddepcontrol.wait. Later stages go weights-then-activations, so the TMA queue never
     // holds a ring's worth of weights in front of the activations the first stage needs.
+    const int pre = min(nst, min(geo.stages, AMSQ_K2_PRE_W));
     if (lane == 0 && nst > 0) {
-      issue_w(0, 0);
+      for (int st = 0; st < pre; ++st) issue_w(st, st);
       for (int st = 1; st < 2 * geo.stages; ++st) prefetch_w(st);  // stages 1 .. 2*ring - 1
     }
     pdl_wait();  // activations may be produced by the previous kernel
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(kK2Threads, AMSQ_CTAS_PER_SM) amsq_linear_kern
     int psidx = -1;
     uint32_t pph = 0;
     for (int st = 0; st < nst; ++st) {
-      if (st > 0) {
+      if (st >= pre) {
         if (st >= geo.stages) {
 #if AMSQ_PRODUCER_SLEEP_NS > 0
           mbar_wait_sleep(&empty[sidx], ph ^ 1u, AMSQ_PRODUCER_SLEEP_NS);
