@@ -240,7 +240,10 @@ int amsq_linear_tp_group(int nranks, const amsq_weight_t* shards, const uint16_t
  * CUDA-graph replayable) then guarantees, in stream order, that this rank's arena holds the
  * whole [batch][N] output at byte offset y_offset. Callers must not overwrite an arena
  * region a peer may still be reading (use distinct offsets per layer, like NCCL user
- * buffers). A peer that never arrives fails the barrier after 2 s (amsq_tp_error). */
+ * buffers). A peer that never arrives fails the barrier after 2 s (amsq_tp_error). The fused
+ * epilogue is K2's: every batch runs K2 (in 32-row chunks), also past the K2/K3 crossover
+ * where amsq_linear_tp would run K3 on the shard -- outputs are within the same bar, not
+ * bit-identical to the K3 path there. */
 typedef struct amsq_tp_s* amsq_tp_t;
 /* One process, every rank's view at once (out[r]); devices may repeat (virtual ranks). */
 int amsq_tp_create_local(int nranks, const int* devices, size_t arena_bytes, amsq_tp_t* out);
