@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 evidence on the committed build: parity (all GPU tests), bench (both schemes) + reference
+# round-end evidence on the working tree: parity (all GPU tests), bench (both schemes) + reference
 # arm, launch list, ncu --set full of K2 (gate_up M=1, o M=1) and K3 (gate_up M=128), SASS listing
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
